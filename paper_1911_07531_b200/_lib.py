@@ -1,0 +1,183 @@
+"""ctypes binding of libhmx.so (include/hmx.h).
+
+The product path has no CPU fallback: importing the engine on a machine
+without the built library raises, and every device entry point raises
+``HmxError`` when the library reports a failure.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._build import LIB
+
+# op codes (hmx_engine.cu)
+OP_NOP, OP_GEMM, OP_COPY, OP_ZERO, OP_ADD, OP_LU, OP_TRSM_LL, OP_TRSM_UT = range(8)
+OP_TRUNC, OP_D2LR, OP_SETRANK, OP_APPEND, OP_SVALS = 8, 9, 10, 11, 12
+F_TA, F_TB, F_ACC = 1, 2, 4
+SCRATCH_BASE = 15
+
+HMX_OK = 0
+HMX_ERR_ARG, HMX_ERR_CUDA, HMX_ERR_PIVOT = 1, 2, 4
+HMX_ERR_RANK_OVERFLOW, HMX_ERR_NOT_CONVERGED, HMX_ERR_TIMEOUT = 8, 16, 32
+
+POLICY_EXACT, POLICY_RANK, POLICY_ACCURACY = 0, 1, 2
+
+OP_DTYPE = np.dtype([
+    ("code", "<i4"), ("flags", "<i4"), ("dim", "<i4", 4), ("ld", "<i4", 4),
+    ("ref", "<i8", 4), ("slot", "<i4", 4), ("iarg", "<i4", 4), ("farg", "<f8", 2),
+    ("wref", "<i8"),
+])
+assert OP_DTYPE.itemsize == 128
+
+
+class HmxError(RuntimeError):
+    def __init__(self, code, what=""):
+        self.code = int(code)
+        names = [n for b, n in ((1, "bad argument"), (2, "CUDA error"), (4, "singular pivot"),
+                                (8, "rank overflow"), (16, "Jacobi not converged"),
+                                (32, "scheduler timeout")) if self.code & b]
+        super().__init__(f"hmx {what}: status {self.code} ({', '.join(names) or 'ok'})")
+
+
+def mref(base: int, off: int) -> int:
+    return (int(base) << 56) | int(off)
+
+
+def slot(base: int, idx: int) -> int:
+    return -(1 + ((int(base) << 24) | int(idx)))
+
+
+class _PlanDesc(C.Structure):
+    _fields_ = [
+        ("ops", C.c_void_p), ("n_ops", C.c_int64),
+        ("task_ops", C.c_void_p), ("n_tasks", C.c_int32),
+        ("succ_ptr", C.c_void_p), ("succ_idx", C.c_void_p),
+        ("wave_ptr", C.c_void_p), ("wave_tasks", C.c_void_p), ("n_waves", C.c_int32),
+        ("scratch_doubles", C.c_int64), ("scratch_ranks", C.c_int32), ("max_ctas", C.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhmx.so; raise if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        raise RuntimeError(f"libhmx.so not built at {LIB}; run __graft_entry__.build()")
+    L = C.CDLL(LIB)
+    vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "hmx_version": ([], C.c_char_p),
+        "hmx_op_size": ([], C.c_int),
+        "hmx_getrf_nopiv_batched": ([i32, i32, vp, i32, i64, vp, vp, i64, vp, vp], i32),
+        "hmx_trsm_lower_unit_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
+        "hmx_trsm_upper_trans_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
+        "hmx_gemm_batched": ([i32, i32, i32, i32, f64, vp, i32, i64, i32, vp, i32, i64, i32, f64,
+                              vp, i32, i64, vp], i32),
+        "hmx_truncate_batched": ([i32, i32, i32, i32, vp, vp, i64, i64, i32, i32, f64, i32, vp, vp,
+                                  i64, i64, vp, vp], i32),
+        "hmx_dense_to_lowrank_batched": ([i32, i32, i32, vp, i64, i32, i32, f64, i32, vp, vp, i64,
+                                          i64, vp, vp], i32),
+        "hmx_svd_values_batched": ([i32, i32, i32, vp, i64, vp, i64, vp], i32),
+        "hmx_plan_create": ([C.POINTER(_PlanDesc), C.POINTER(vp)], i32),
+        "hmx_plan_bind": ([vp, i32, vp, vp], i32),
+        "hmx_plan_execute": ([vp, i32, vp], i32),
+        "hmx_plan_status": ([vp, vp, C.POINTER(i32)], i32),
+        "hmx_plan_counters": ([vp, vp, C.POINTER(C.c_uint64)], i32),
+        "hmx_plan_reset_counters": ([vp, vp], i32),
+        "hmx_plan_destroy": ([vp], i32),
+        "hmx_exp_kernel_blocks": ([i32, vp, vp, i32, vp, f64, f64, f64, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.hmx_op_size() != OP_DTYPE.itemsize:
+        raise RuntimeError("libhmx.so op record size mismatch")
+    _lib = L
+    return L
+
+
+EXPORTED = (
+    "hmx_version", "hmx_op_size", "hmx_getrf_nopiv_batched", "hmx_trsm_lower_unit_batched",
+    "hmx_trsm_upper_trans_batched", "hmx_gemm_batched", "hmx_truncate_batched",
+    "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
+    "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
+    "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_exp_kernel_blocks",
+)
+
+
+def check(status, what=""):
+    if status != HMX_OK:
+        raise HmxError(status, what)
+
+
+def stream_ptr(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+class Plan:
+    """Owning handle of a device execution plan (hmx_plan_t)."""
+
+    def __init__(self, ops, task_ops, succ_ptr, succ_idx, wave_ptr, wave_tasks,
+                 scratch_doubles, scratch_ranks, max_ctas=0):
+        L = lib()
+        self._keep = [np.ascontiguousarray(ops, dtype=OP_DTYPE),
+                      np.ascontiguousarray(task_ops, dtype=np.int64),
+                      np.ascontiguousarray(succ_ptr, dtype=np.int32),
+                      np.ascontiguousarray(succ_idx, dtype=np.int32),
+                      np.ascontiguousarray(wave_ptr, dtype=np.int32),
+                      np.ascontiguousarray(wave_tasks, dtype=np.int32)]
+        o, to, sp, si, wp, wt = self._keep
+        d = _PlanDesc(o.ctypes.data, len(o), to.ctypes.data, len(to) - 1, sp.ctypes.data,
+                      si.ctypes.data, wp.ctypes.data, wt.ctypes.data, len(wp) - 1,
+                      int(scratch_doubles), int(scratch_ranks), int(max_ctas))
+        h = C.c_void_p()
+        check(L.hmx_plan_create(C.byref(d), C.byref(h)), "plan_create")
+        self.h = h
+        self._keep = None
+        self.n_tasks = len(to) - 1
+
+    def bind(self, base_id, values, ranks=None):
+        check(lib().hmx_plan_bind(self.h, int(base_id), ptr(values), ptr(ranks)), "plan_bind")
+
+    def execute(self, mode=2, stream=None):
+        check(lib().hmx_plan_execute(self.h, int(mode), stream_ptr(stream)), "plan_execute")
+
+    def status(self, stream=None) -> int:
+        v = C.c_int32()
+        check(lib().hmx_plan_status(self.h, stream_ptr(stream), C.byref(v)), "plan_status")
+        return int(v.value)
+
+    def counters(self, stream=None):
+        arr = (C.c_uint64 * 4)()
+        check(lib().hmx_plan_counters(self.h, stream_ptr(stream), arr), "plan_counters")
+        return [int(x) for x in arr]
+
+    def reset_counters(self, stream=None):
+        check(lib().hmx_plan_reset_counters(self.h, stream_ptr(stream)), "plan_reset")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hmx_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

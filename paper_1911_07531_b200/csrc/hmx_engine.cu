@@ -1,0 +1,989 @@
+// hmx_engine.cu — op-program interpreter, DAG executors and the C ABI.
+//
+// The host planner (planner.py) lowers every final task of the refined
+// H-LU DAG (taskgraph.build_hlu_dag, taskgraph.py:636-665) to a contiguous
+// range of hmx_op records.  One CTA executes one task: it walks the task's
+// ops in order, each op being a CTA-cooperative fp64 routine from
+// hmx_device.cuh.  Ranks produced by truncations live in device rank slots,
+// so the task programs are fixed at plan time and no host round trip is
+// needed between tasks.
+//
+// Executors (hmx_plan_execute):
+//   0 wave       one launch per ASAP wavefront of the dependency graph
+//   1 graph      the same launches captured once into a CUDA graph
+//   2 persistent one launch; CTAs pop ready tasks from a device queue and
+//                release successors through per-task dependency counters
+//   3 sequential one task per launch in program order (debug / oracle order)
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include <initializer_list>
+
+#include "../../include/hmx.h"
+#include "hmx_device.cuh"
+
+using namespace hmx;
+
+namespace {
+
+enum OpCode : int32_t {
+  OP_NOP = 0,
+  OP_GEMM = 1,      // C[m x n] (+)= alpha op(A)[m x k] op(B)[k x n]
+  OP_COPY = 2,      // C[m x n] = alpha op(A)
+  OP_ZERO = 3,      // C[m x n] = 0
+  OP_ADD = 4,       // C[m x n] += alpha A
+  OP_LU = 5,        // A[n x n] -> L, U            (arith.dense_lu)
+  OP_TRSM_LL = 6,   // B[n x c] := L^{-1} B        (solve_triangular lower, unit)
+  OP_TRSM_UT = 7,   // B[n x c] := U^{-T} B        (solve_triangular trans)
+  OP_TRUNC = 8,     // (U[m x K], V[n x K]) -> (U', V', r)   (hmatrix.truncate)
+  OP_D2LR = 9,      // M[m x n] -> (U', V', r)   (hmatrix.dense_to_lowrank)
+  OP_SETRANK = 10,  // slot0 := dim0
+  OP_APPEND = 11,   // hstack with zero padding (hmatrix.py:404-409,435-436)
+  OP_SVALS = 12     // sigma of G[p x q] (test entry point)
+};
+
+enum : int32_t { F_TA = 1, F_TB = 2, F_ACC = 4 };
+
+constexpr int kScratchBase = 15;
+constexpr int kSmemDoubles = 12288;  // 96 KB dynamic shared memory per CTA
+constexpr int kSmemWork = kSmemDoubles - 32;
+
+struct DevPlan {
+  const hmx_op* ops;
+  const int64_t* task_ops;
+  double* bases[16];
+  int* rbases[16];
+  double* scratch;
+  int64_t scratch_stride;
+  int* rscratch;
+  int rscratch_stride;
+  unsigned long long* counters;  // [0] trunc [1] flops [2] bytes [3] tasks
+  int* status;
+  // persistent scheduler
+  int* indeg;
+  const int* succ_ptr;
+  const int* succ_idx;
+  int* queue;
+  int* qctl;  // [0] head, [1] tail
+  int n_tasks;
+};
+
+struct Cx {
+  double* scratch;
+  int* rscratch;
+};
+
+__device__ __forceinline__ double* mref(const DevPlan& P, const Cx& c, int64_t r) {
+  const int b = (int)((uint64_t)r >> 56);
+  const int64_t off = r & ((1LL << 56) - 1);
+  return (b == kScratchBase ? c.scratch : P.bases[b]) + off;
+}
+
+__device__ __forceinline__ int* slotp(const DevPlan& P, const Cx& c, int32_t code) {
+  const int s = -code - 1;
+  const int b = s >> 24, i = s & 0xFFFFFF;
+  return (b == kScratchBase ? c.rscratch : P.rbases[b]) + i;
+}
+
+__device__ __forceinline__ int dimv(const DevPlan& P, const Cx& c, int32_t code) {
+  if (code >= 0) return code;
+  return *slotp(P, c, code);
+}
+
+__device__ __forceinline__ void set_status(const DevPlan& P, int bits) {
+  atomicOr(P.status, bits);
+}
+
+__device__ __forceinline__ void count(const DevPlan& P, double flops, double bytes) {
+  if (threadIdx.x == 0) {
+    atomicAdd(&P.counters[1], (unsigned long long)flops);
+    atomicAdd(&P.counters[2], (unsigned long long)bytes);
+  }
+}
+
+// SURVEY.md §8d formulas
+__device__ __forceinline__ double qr_flops(double m, double k) {
+  return 2.0 * (2.0 * m * k * k - 2.0 * k * k * k / 3.0);
+}
+__device__ __forceinline__ double svd_flops(double m, double n) {
+  const double l = fmax(m, n), s = fmin(m, n);
+  return 4.0 * l * s * s + 22.0 * s * s * s;
+}
+
+// ---------------------------------------------------------------------------
+// truncate (hmatrix.py:113-130)
+// ---------------------------------------------------------------------------
+__device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
+  const int m = o.dim[0], n = o.dim[1];
+  const int K = dimv(P, c, o.dim[2]);
+  int* rslot = slotp(P, c, o.slot[0]);
+  if (K == 0) {  // rank-0 passthrough, not counted (hmatrix.py:121-122)
+    if (threadIdx.x == 0) *rslot = 0;
+    __syncthreads();
+    return;
+  }
+  if (threadIdx.x == 0) atomicAdd(&P.counters[0], 1ull);
+  double* U = mref(P, c, o.ref[0]);
+  double* V = mref(P, c, o.ref[1]);
+  double* Uo = mref(P, c, o.ref[2]);
+  double* Vo = mref(P, c, o.ref[3]);
+  const int ldu = o.ld[0], ldv = o.ld[1], lduo = o.ld[2], ldvo = o.ld[3];
+  const int kcap = o.iarg[3];
+  double* ws = mref(P, c, o.wref);
+  double* tau_u = ws;
+  double* tau_v = ws + kcap;
+  double* sig = ws + 2 * kcap;
+  int* ord = reinterpret_cast<int*>(ws + 3 * kcap);
+  double* gws = ws + 4 * kcap;  // G (kcap*kcap) then J (kcap*kcap)
+  double* red = sm;
+  int* flag = reinterpret_cast<int*>(sm + 8);
+  double* work = sm + 32;
+
+  cta_householder_qr(m, K, U, ldu, tau_u, red);
+  cta_householder_qr(n, K, V, ldv, tau_v, red);
+  const int p = min(m, K), q = min(n, K);
+  const bool tr = q > p;                 // Jacobi over the shorter side
+  const int gr = tr ? q : p, gc = tr ? p : q;  // G' is gr x gc, J is gc x gc
+  double *G, *J;
+  if (gr * gc + gc * gc <= kSmemWork) { G = work; J = work + gr * gc; }
+  else { G = gws; J = gws + (int64_t)kcap * kcap; }
+  // G = Ru Rv^T (p x q), or its transpose
+  for (int e = threadIdx.x; e < p * q; e += HMX_THREADS) {
+    const int i = e % p, j = e / p;
+    double s = 0.0;
+    for (int l = max(i, j); l < K; ++l) s = fma(U[i + (int64_t)l * ldu], V[j + (int64_t)l * ldv], s);
+    if (!tr) G[i + j * gr] = s; else G[j + i * gr] = s;
+  }
+  __syncthreads();
+  if (!cta_jacobi_svd(gr, gc, G, gr, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
+  const int size = gc;  // = min(p, q)
+  int r = keep_count(o.iarg[0], o.iarg[1], o.farg[1], sig, ord, size);
+  const int cap = o.iarg[2];
+  if (r > cap) { if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW); r = cap; }
+  // Y_U -> Uo (m x r), Y_V -> Vo (n x r)
+  for (int e = threadIdx.x; e < m * r; e += HMX_THREADS) {
+    const int i = e % m, t = e / m;
+    const int col = ord[t];
+    double v = 0.0;
+    if (i < p) v = !tr ? G[i + col * gr] : J[i + col * gc] * sig[col];
+    Uo[i + (int64_t)t * lduo] = v;
+  }
+  for (int e = threadIdx.x; e < n * r; e += HMX_THREADS) {
+    const int i = e % n, t = e / n;
+    const int col = ord[t];
+    double v = 0.0;
+    if (i < q) v = !tr ? J[i + col * gc] : G[i + col * gr] / sig[col];
+    Vo[i + (int64_t)t * ldvo] = v;
+  }
+  __syncthreads();
+  cta_apply_q(m, p, U, ldu, tau_u, r, Uo, lduo);
+  cta_apply_q(n, q, V, ldv, tau_v, r, Vo, ldvo);
+  if (threadIdx.x == 0) *rslot = r;
+  count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) +
+               2.0 * m * p * r + 2.0 * n * q * r,
+        8.0 * (2.0 * m * K + 2.0 * n * K + (double)K * K + (m + n) * (double)r));
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// dense_to_lowrank (hmatrix.py:133-138)
+// ---------------------------------------------------------------------------
+__device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
+  const int m = o.dim[0], n = o.dim[1];
+  int* rslot = slotp(P, c, o.slot[0]);
+  if (threadIdx.x == 0) atomicAdd(&P.counters[0], 1ull);
+  double* M = mref(P, c, o.ref[0]);
+  const int ldm = o.ld[0];
+  double* Uo = mref(P, c, o.ref[2]);
+  double* Vo = mref(P, c, o.ref[3]);
+  const int lduo = o.ld[2], ldvo = o.ld[3];
+  double* ws = mref(P, c, o.wref);
+  const int s = min(m, n);
+  const bool tr = n > m;
+  const int gr = tr ? n : m, gc = tr ? m : n;
+  double* sig = ws;
+  int* ord = reinterpret_cast<int*>(ws + s);
+  double* gws = ws + 2 * s;
+  int* flag = reinterpret_cast<int*>(sm + 8);
+  double* work = sm + 32;
+  double *G, *J;
+  int ldg;
+  if (gr * gc + gc * gc <= kSmemWork) { G = work; J = work + gr * gc; ldg = gr; }
+  else if (!tr) { G = M; ldg = ldm; J = gws; }
+  else { G = gws + (int64_t)gc * gc; J = gws; ldg = gr; }
+  if (G != M) {
+    for (int e = threadIdx.x; e < gr * gc; e += HMX_THREADS) {
+      const int i = e % gr, j = e / gr;
+      G[i + j * ldg] = !tr ? M[i + (int64_t)j * ldm] : M[j + (int64_t)i * ldm];
+    }
+    __syncthreads();
+  }
+  if (!cta_jacobi_svd(gr, gc, G, ldg, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
+  int r = keep_count(o.iarg[0], o.iarg[1], o.farg[1], sig, ord, s);
+  const int cap = o.iarg[2];
+  if (r > cap) { if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW); r = cap; }
+  for (int e = threadIdx.x; e < m * r; e += HMX_THREADS) {
+    const int i = e % m, t = e / m, col = ord[t];
+    Uo[i + (int64_t)t * lduo] = !tr ? G[i + (int64_t)col * ldg] : J[i + col * gc] * sig[col];
+  }
+  for (int e = threadIdx.x; e < n * r; e += HMX_THREADS) {
+    const int i = e % n, t = e / n, col = ord[t];
+    Vo[i + (int64_t)t * ldvo] = !tr ? J[i + col * gc] : G[i + (int64_t)col * ldg] / sig[col];
+  }
+  if (threadIdx.x == 0) *rslot = r;
+  count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s + (double)s * n));
+  __syncthreads();
+}
+
+__device__ void op_svals(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
+  const int p = o.dim[0], q = o.dim[1];
+  double* G = mref(P, c, o.ref[0]);
+  double* out = mref(P, c, o.ref[2]);
+  double* ws = mref(P, c, o.wref);
+  const bool tr = q > p;
+  const int gr = tr ? q : p, gc = tr ? p : q;
+  double* J = ws;
+  double* W = ws + (int64_t)gc * gc;
+  double* sig = W + (int64_t)gr * gc;
+  int* ord = reinterpret_cast<int*>(sig + gc);
+  int* flag = reinterpret_cast<int*>(sm + 8);
+  for (int e = threadIdx.x; e < gr * gc; e += HMX_THREADS) {
+    const int i = e % gr, j = e / gr;
+    W[i + (int64_t)j * gr] = !tr ? G[i + (int64_t)j * o.ld[0]] : G[j + (int64_t)i * o.ld[0]];
+  }
+  __syncthreads();
+  if (!cta_jacobi_svd(gr, gc, W, gr, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
+  for (int t = threadIdx.x; t < gc; t += HMX_THREADS) out[t] = sig[ord[t]];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// one op
+// ---------------------------------------------------------------------------
+__device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
+  double* red = sm;
+  double* work = sm + 32;
+  switch (o.code) {
+    case OP_GEMM: {
+      const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]), k = dimv(P, c, o.dim[2]);
+      const bool acc = o.flags & F_ACC;
+      if (m == 0 || n == 0) break;
+      double* C = mref(P, c, o.ref[2]);
+      if (k == 0) {
+        if (!acc) { cta_zero(m, n, C, o.ld[2]); __syncthreads(); }
+        break;
+      }
+      cta_gemm(m, n, k, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
+               mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
+      count(P, 2.0 * m * n * k, 8.0 * ((double)m * k + (double)k * n + (double)m * n));
+      break;
+    }
+    case OP_COPY: {
+      const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]);
+      cta_copy(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
+               mref(P, c, o.ref[2]), o.ld[2]);
+      __syncthreads();
+      break;
+    }
+    case OP_ZERO: {
+      const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]);
+      cta_zero(m, n, mref(P, c, o.ref[2]), o.ld[2]);
+      __syncthreads();
+      break;
+    }
+    case OP_ADD: {
+      const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]);
+      cta_add(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], mref(P, c, o.ref[2]), o.ld[2]);
+      __syncthreads();
+      break;
+    }
+    case OP_LU: {
+      const int n = o.dim[0];
+      double* U = mref(P, c, o.ref[2]);
+      double* W = (n * n + n <= kSmemWork) ? work + n : U;
+      const bool ok = cta_lu(n, mref(P, c, o.ref[0]), o.ld[0], mref(P, c, o.ref[1]), o.ld[1], U,
+                             o.ld[2], W, work, red);
+      if (!ok && threadIdx.x == 0) set_status(P, HMX_ERR_PIVOT);
+      count(P, 2.0 / 3.0 * n * n * (double)n, 16.0 * n * n);
+      break;
+    }
+    case OP_TRSM_LL:
+    case OP_TRSM_UT: {
+      const int n = o.dim[0], cc = dimv(P, c, o.dim[1]);
+      if (cc == 0 || n == 0) break;
+      const double* T = mref(P, c, o.ref[0]);
+      int ldt = o.ld[0];
+      double* B = mref(P, c, o.ref[2]);
+      int ldb = o.ld[2];
+      double* Ts = work;
+      const bool stageT = n * n <= kSmemWork;
+      if (stageT) {
+        for (int e = threadIdx.x; e < n * n; e += HMX_THREADS)
+          Ts[e] = T[(e % n) + (int64_t)(e / n) * ldt];
+        T = Ts;
+        ldt = n;
+      }
+      double* Bs = work + (stageT ? n * n : 0);
+      const bool stageB = stageT && (n * n + n * cc <= kSmemWork);
+      if (stageB)
+        for (int e = threadIdx.x; e < n * cc; e += HMX_THREADS)
+          Bs[e] = B[(e % n) + (int64_t)(e / n) * ldb];
+      __syncthreads();
+      double* Bw = stageB ? Bs : B;
+      const int ldw = stageB ? n : ldb;
+      if (o.code == OP_TRSM_LL) cta_trsm_lower_unit(n, cc, T, ldt, Bw, ldw);
+      else cta_trsm_upper_trans(n, cc, T, ldt, Bw, ldw);
+      if (stageB) {
+        for (int e = threadIdx.x; e < n * cc; e += HMX_THREADS)
+          B[(e % n) + (int64_t)(e / n) * ldb] = Bs[e];
+        __syncthreads();
+      }
+      count(P, (double)n * n * cc, 8.0 * ((double)n * n / 2.0 + 2.0 * n * cc));
+      break;
+    }
+    case OP_TRUNC: op_trunc(P, c, o, sm); break;
+    case OP_D2LR: op_d2lr(P, c, o, sm); break;
+    case OP_SVALS: op_svals(P, c, o, sm); break;
+    case OP_SETRANK: {
+      const int v = dimv(P, c, o.dim[0]);
+      __syncthreads();
+      if (threadIdx.x == 0) *slotp(P, c, o.slot[0]) = v;
+      __syncthreads();
+      break;
+    }
+    case OP_APPEND: {
+      // dst U (M x capc, ld ld2) and V (N x capc, ld ld3) get k new columns at
+      // column offset *slot0: rows r0.. (c0..) hold the source, the rest 0.
+      const int M = o.dim[0], N = o.dim[1], k = dimv(P, c, o.dim[2]), capc = o.dim[3];
+      const int mq = o.iarg[0], nq = o.iarg[1], r0 = o.iarg[2], c0 = o.iarg[3];
+      int* cnt = slotp(P, c, o.slot[0]);
+      const int col0 = *cnt;
+      __syncthreads();
+      if (col0 + k > capc) {
+        if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW);
+        __syncthreads();
+        break;
+      }
+      const double* Us = mref(P, c, o.ref[0]);
+      const double* Vs = mref(P, c, o.ref[1]);
+      double* Ud = mref(P, c, o.ref[2]) + (int64_t)col0 * o.ld[2];
+      double* Vd = mref(P, c, o.ref[3]) + (int64_t)col0 * o.ld[3];
+      for (int e = threadIdx.x; e < M * k; e += HMX_THREADS) {
+        const int i = e % M, t = e / M;
+        Ud[i + (int64_t)t * o.ld[2]] =
+            (i >= r0 && i < r0 + mq) ? Us[(i - r0) + (int64_t)t * o.ld[0]] : 0.0;
+      }
+      for (int e = threadIdx.x; e < N * k; e += HMX_THREADS) {
+        const int i = e % N, t = e / N;
+        Vd[i + (int64_t)t * o.ld[3]] =
+            (i >= c0 && i < c0 + nq) ? Vs[(i - c0) + (int64_t)t * o.ld[1]] : 0.0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) *cnt = col0 + k;
+      __syncthreads();
+      break;
+    }
+    default: break;
+  }
+}
+
+__device__ void run_task(const DevPlan& P, int t, double* sm) {
+  Cx c;
+  c.scratch = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
+  c.rscratch = P.rscratch + (int64_t)blockIdx.x * P.rscratch_stride;
+  const int64_t b = P.task_ops[t], e = P.task_ops[t + 1];
+  for (int64_t i = b; i < e; ++i) {
+    const hmx_op o = P.ops[i];
+    run_op(P, c, o, sm);
+  }
+  if (threadIdx.x == 0) atomicAdd(&P.counters[3], 1ull);
+}
+
+__global__ void __launch_bounds__(HMX_THREADS) k_tasks(DevPlan P, const int* tasks, int ntasks) {
+  extern __shared__ double sm[];
+  for (int i = blockIdx.x; i < ntasks; i += gridDim.x) {
+    run_task(P, tasks ? tasks[i] : i, sm);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int ld_relaxed(int* p) { return atomicAdd(p, 0); }
+
+__global__ void __launch_bounds__(HMX_THREADS) k_persistent(DevPlan P) {
+  extern __shared__ double sm[];
+  __shared__ int s_task;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int slot = atomicAdd(&P.qctl[0], 1);
+      int t = -1;
+      if (slot < P.n_tasks) {
+        long long spins = 0;
+        while ((t = ld_relaxed(&P.queue[slot])) < 0) {
+          __nanosleep(128);
+          if (++spins > (1ll << 27)) { atomicOr(P.status, HMX_ERR_TIMEOUT); t = -2; break; }
+          if ((spins & 1023) == 0 && (ld_relaxed(P.status) & HMX_ERR_TIMEOUT)) { t = -2; break; }
+        }
+      }
+      s_task = t;
+    }
+    __syncthreads();
+    const int t = s_task;
+    if (t < 0) break;
+    __threadfence();  // acquire: invalidate L1 before reading predecessors' outputs
+    run_task(P, t, sm);
+    __threadfence();  // release this task's outputs (every writer thread)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int k = P.succ_ptr[t]; k < P.succ_ptr[t + 1]; ++k) {
+        const int s = P.succ_idx[k];
+        if (atomicSub(&P.indeg[s], 1) == 1) {
+          const int pos = atomicAdd(&P.qctl[1], 1);
+          atomicExch(&P.queue[pos], s);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_exp_kernel(int nblocks, const int64_t* desc, const double* pts, int dim,
+                             const int64_t* perm, double ell, double diag, double scale,
+                             double* out) {
+  const int b = blockIdx.y;
+  if (b >= nblocks) return;
+  const int64_t r0 = desc[5 * b], m = desc[5 * b + 1], c0 = desc[5 * b + 2], n = desc[5 * b + 3];
+  double* o = out + desc[5 * b + 4];
+  const int64_t tot = m * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    const int64_t pi = perm[r0 + i], pj = perm[c0 + j];
+    double v;
+    if (pi == pj) v = diag;
+    else {
+      double s = 0.0;
+      for (int d = 0; d < dim; ++d) {
+        const double t = pts[pi * dim + d] - pts[pj * dim + d];
+        s += t * t;
+      }
+      v = scale * exp(-sqrt(s) / ell);
+    }
+    o[i + j * m] = v;
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+bool g_attr_set = false;
+cudaError_t set_attrs() {
+  if (g_attr_set) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemDoubles * (int)sizeof(double));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemDoubles * (int)sizeof(double));
+  if (e != cudaSuccess) return e;
+  g_attr_set = true;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+// ===========================================================================
+// plans
+// ===========================================================================
+struct hmx_plan {
+  int n_tasks = 0, n_waves = 0;
+  int64_t n_ops = 0;
+  hmx_op* d_ops = nullptr;
+  int64_t* d_task_ops = nullptr;
+  int* d_succ_ptr = nullptr;
+  int* d_succ_idx = nullptr;
+  int* d_indeg_init = nullptr;
+  int* d_indeg = nullptr;
+  int* d_queue_init = nullptr;
+  int* d_queue = nullptr;
+  int* d_qctl = nullptr;
+  int qctl_init[2] = {0, 0};
+  std::vector<int> wave_ptr;
+  int* d_wave_tasks = nullptr;
+  int* d_seq_tasks = nullptr;
+  int max_wave = 0;
+  double* d_scratch = nullptr;
+  int* d_rscratch = nullptr;
+  int64_t scratch_stride = 0;
+  int rscratch_stride = 0;
+  int n_ctas = 0;
+  unsigned long long* d_counters = nullptr;
+  int* d_status = nullptr;
+  double* bases[16] = {};
+  int* rbases[16] = {};
+  cudaGraphExec_t gexec = nullptr;
+};
+
+namespace {
+
+template <class T>
+cudaError_t upload(T** dst, const T* src, size_t n) {
+  cudaError_t e = cudaMalloc((void**)dst, std::max<size_t>(n, 1) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (n) e = cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+DevPlan make_dev(hmx_plan* p) {
+  DevPlan P;
+  memset(&P, 0, sizeof(P));
+  P.ops = p->d_ops;
+  P.task_ops = p->d_task_ops;
+  for (int i = 0; i < 16; ++i) { P.bases[i] = p->bases[i]; P.rbases[i] = p->rbases[i]; }
+  P.scratch = p->d_scratch;
+  P.scratch_stride = p->scratch_stride;
+  P.rscratch = p->d_rscratch;
+  P.rscratch_stride = p->rscratch_stride;
+  P.counters = p->d_counters;
+  P.status = p->d_status;
+  P.indeg = p->d_indeg;
+  P.succ_ptr = p->d_succ_ptr;
+  P.succ_idx = p->d_succ_idx;
+  P.queue = p->d_queue;
+  P.qctl = p->d_qctl;
+  P.n_tasks = p->n_tasks;
+  return P;
+}
+
+hmx_status cuda_status(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[hmx] CUDA error: %s\n", cudaGetErrorString(e));
+    return HMX_ERR_CUDA;
+  }
+  return HMX_OK;
+}
+
+cudaError_t launch_waves(hmx_plan* p, cudaStream_t s) {
+  DevPlan P = make_dev(p);
+  const size_t smem = kSmemDoubles * sizeof(double);
+  for (int w = 0; w < p->n_waves; ++w) {
+    const int b = p->wave_ptr[w], n = p->wave_ptr[w + 1] - b;
+    if (!n) continue;
+    const int grid = std::min(n, p->n_ctas);
+    k_tasks<<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hmx_version(void) { return "hmx 0.1 sm_100a fp64"; }
+int hmx_op_size(void) { return (int)sizeof(hmx_op); }
+
+hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
+  if (!d || !out || d->n_tasks < 0) return HMX_ERR_ARG;
+  cudaError_t e = set_attrs();
+  if (e != cudaSuccess) return cuda_status(e);
+  hmx_plan* p = new hmx_plan();
+  p->n_tasks = d->n_tasks;
+  p->n_ops = d->n_ops;
+  p->n_waves = d->n_waves;
+  const int nt = d->n_tasks;
+  e = upload(&p->d_ops, d->ops, (size_t)d->n_ops);
+  if (!e) e = upload(&p->d_task_ops, d->task_ops, (size_t)nt + 1);
+  if (!e) e = upload(&p->d_succ_ptr, d->succ_ptr, (size_t)nt + 1);
+  const int ne = d->succ_ptr[nt];
+  if (!e) e = upload(&p->d_succ_idx, d->succ_idx, (size_t)ne);
+  std::vector<int> indeg(nt, 0);
+  for (int i = 0; i < ne; ++i) indeg[d->succ_idx[i]]++;
+  std::vector<int> queue(nt, -1);
+  int r = 0;
+  // seed the ready queue in wave order (wave 0 = the zero in-degree tasks)
+  for (int i = 0; i < nt; ++i) {
+    const int t = d->wave_tasks[i];
+    if (indeg[t] == 0) queue[r++] = t;
+  }
+  p->qctl_init[0] = 0;
+  p->qctl_init[1] = r;
+  if (!e) e = upload(&p->d_indeg_init, indeg.data(), (size_t)nt);
+  if (!e) e = cudaMalloc(&p->d_indeg, std::max(nt, 1) * sizeof(int));
+  if (!e) e = upload(&p->d_queue_init, queue.data(), (size_t)nt);
+  if (!e) e = cudaMalloc(&p->d_queue, std::max(nt, 1) * sizeof(int));
+  if (!e) e = cudaMalloc(&p->d_qctl, 2 * sizeof(int));
+  p->wave_ptr.assign(d->wave_ptr, d->wave_ptr + d->n_waves + 1);
+  for (int w = 0; w < d->n_waves; ++w)
+    p->max_wave = std::max(p->max_wave, p->wave_ptr[w + 1] - p->wave_ptr[w]);
+  if (!e) e = upload(&p->d_wave_tasks, d->wave_tasks, (size_t)nt);
+  std::vector<int> seq(nt);
+  for (int i = 0; i < nt; ++i) seq[i] = i;
+  if (!e) e = upload(&p->d_seq_tasks, seq.data(), (size_t)nt);
+  p->n_ctas = d->max_ctas > 0 ? d->max_ctas : 2 * num_sms();
+  p->scratch_stride = std::max<int64_t>(d->scratch_doubles, 1);
+  p->scratch_stride = (p->scratch_stride + 31) & ~int64_t(31);
+  p->rscratch_stride = std::max(d->scratch_ranks, 1);
+  if (!e) e = cudaMalloc(&p->d_scratch, (size_t)p->scratch_stride * p->n_ctas * sizeof(double));
+  if (!e) e = cudaMalloc(&p->d_rscratch, (size_t)p->rscratch_stride * p->n_ctas * sizeof(int));
+  if (!e) e = cudaMalloc(&p->d_counters, 4 * sizeof(unsigned long long));
+  if (!e) e = cudaMemset(p->d_counters, 0, 4 * sizeof(unsigned long long));
+  if (!e) e = cudaMalloc(&p->d_status, sizeof(int));
+  if (!e) e = cudaMemset(p->d_status, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    hmx_plan_destroy(p);
+    return cuda_status(e);
+  }
+  *out = p;
+  return HMX_OK;
+}
+
+hmx_status hmx_plan_bind(hmx_plan_t p, int32_t base_id, double* values, int32_t* ranks) {
+  if (!p || base_id < 0 || base_id >= 15) return HMX_ERR_ARG;
+  p->bases[base_id] = values;
+  p->rbases[base_id] = ranks;
+  if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+  return HMX_OK;
+}
+
+hmx_status hmx_plan_execute(hmx_plan_t p, int32_t mode, void* stream) {
+  if (!p) return HMX_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->n_tasks == 0) return HMX_OK;
+  const size_t smem = kSmemDoubles * sizeof(double);
+  cudaError_t e = cudaSuccess;
+  if (mode == 0) {
+    e = launch_waves(p, s);
+  } else if (mode == 1) {
+    if (!p->gexec) {
+      cudaStream_t cs;
+      e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+      if (e) return cuda_status(e);
+      cudaGraph_t g;
+      e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+      if (!e) {
+        launch_waves(p, cs);
+        e = cudaStreamEndCapture(cs, &g);
+      }
+      if (!e) {
+        e = cudaGraphInstantiate(&p->gexec, g, 0);
+        cudaGraphDestroy(g);
+      }
+      cudaStreamDestroy(cs);
+      if (e) return cuda_status(e);
+    }
+    e = cudaGraphLaunch(p->gexec, s);
+  } else if (mode == 2) {
+    e = cudaMemcpyAsync(p->d_indeg, p->d_indeg_init, p->n_tasks * sizeof(int),
+                        cudaMemcpyDeviceToDevice, s);
+    if (!e) e = cudaMemcpyAsync(p->d_queue, p->d_queue_init, p->n_tasks * sizeof(int),
+                                cudaMemcpyDeviceToDevice, s);
+    if (!e) e = cudaMemcpyAsync(p->d_qctl, p->qctl_init, 2 * sizeof(int), cudaMemcpyHostToDevice, s);
+    if (!e) {
+      DevPlan P = make_dev(p);
+      k_persistent<<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
+      e = cudaGetLastError();
+    }
+  } else if (mode == 3) {
+    DevPlan P = make_dev(p);
+    for (int t = 0; t < p->n_tasks && !e; ++t) {
+      k_tasks<<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
+      e = cudaGetLastError();
+    }
+  } else {
+    return HMX_ERR_ARG;
+  }
+  return cuda_status(e);
+}
+
+hmx_status hmx_plan_status(hmx_plan_t p, void* stream, int32_t* bits) {
+  if (!p || !bits) return HMX_ERR_ARG;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (!e) e = cudaMemcpy(bits, p->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+  return cuda_status(e);
+}
+
+hmx_status hmx_plan_counters(hmx_plan_t p, void* stream, uint64_t out[4]) {
+  if (!p || !out) return HMX_ERR_ARG;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (!e) e = cudaMemcpy(out, p->d_counters, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  return cuda_status(e);
+}
+
+hmx_status hmx_plan_reset_counters(hmx_plan_t p, void* stream) {
+  if (!p) return HMX_ERR_ARG;
+  cudaError_t e = cudaMemsetAsync(p->d_counters, 0, 4 * sizeof(unsigned long long),
+                                  (cudaStream_t)stream);
+  if (!e) e = cudaMemsetAsync(p->d_status, 0, sizeof(int), (cudaStream_t)stream);
+  return cuda_status(e);
+}
+
+hmx_status hmx_plan_destroy(hmx_plan_t p) {
+  if (!p) return HMX_OK;
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  void* ptrs[] = {p->d_ops, p->d_task_ops, p->d_succ_ptr, p->d_succ_idx, p->d_indeg_init,
+                  p->d_indeg, p->d_queue_init, p->d_queue, p->d_qctl, p->d_wave_tasks,
+                  p->d_seq_tasks, p->d_scratch, p->d_rscratch, p->d_counters, p->d_status};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete p;
+  return HMX_OK;
+}
+
+hmx_status hmx_exp_kernel_blocks(int32_t nblocks, const int64_t* desc, const double* points,
+                                 int32_t dim, const int64_t* perm, double ell, double diag,
+                                 double scale, double* out, void* stream) {
+  if (nblocks <= 0) return HMX_OK;
+  dim3 grid(64, nblocks);
+  k_exp_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(nblocks, desc, points, dim, perm, ell, diag,
+                                                       scale, out);
+  return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// batched leaf-kernel entry points: each batch entry becomes a one-task op
+// program run by the same interpreter as the H-LU plans.
+// ===========================================================================
+namespace {
+
+constexpr int kBaseIn = 0, kBaseOut = 1, kBaseOut2 = 2, kBaseRank = 3, kBaseOut3 = 4;
+
+inline int64_t R(int base, int64_t off) { return ((int64_t)base << 56) | off; }
+inline int32_t S(int base, int idx) { return -(1 + ((base << 24) | idx)); }
+
+struct MiniRun {
+  std::vector<hmx_op> ops;
+  std::vector<int64_t> task_ops{0};
+  void end_task() { task_ops.push_back((int64_t)ops.size()); }
+};
+
+struct Bind { int id; double* v; int* r; };
+
+hmx_status run_mini(MiniRun& mr, std::initializer_list<Bind> binds, int64_t scratch, int nranks,
+                    cudaStream_t s, int* status_out = nullptr) {
+  hmx_plan_desc d;
+  memset(&d, 0, sizeof(d));
+  const int nt = (int)mr.task_ops.size() - 1;
+  std::vector<int> succ_ptr(nt + 1, 0), waves(nt), wave_ptr{0, nt};
+  for (int i = 0; i < nt; ++i) waves[i] = i;
+  d.ops = mr.ops.data();
+  d.n_ops = (int64_t)mr.ops.size();
+  d.task_ops = mr.task_ops.data();
+  d.n_tasks = nt;
+  d.succ_ptr = succ_ptr.data();
+  d.succ_idx = nullptr;
+  d.wave_ptr = wave_ptr.data();
+  d.wave_tasks = waves.data();
+  d.n_waves = 1;
+  d.scratch_doubles = scratch;
+  d.scratch_ranks = nranks;
+  hmx_plan_t p;
+  hmx_status st = hmx_plan_create(&d, &p);
+  if (st) return st;
+  for (const Bind& b : binds) hmx_plan_bind(p, b.id, b.v, b.r);
+  st = hmx_plan_execute(p, 0, s);
+  int bits = 0;
+  if (!st) st = hmx_plan_status(p, s, &bits);
+  hmx_plan_destroy(p);
+  if (status_out) *status_out = bits;
+  if (st) return st;
+  return bits ? bits : HMX_OK;
+}
+
+hmx_op blank(int code) {
+  hmx_op o;
+  memset(&o, 0, sizeof(o));
+  o.code = code;
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+hmx_status hmx_getrf_nopiv_batched(int32_t batch, int32_t n, const double* A, int32_t lda,
+                                   int64_t strideA, double* L, double* U, int64_t strideLU,
+                                   int32_t* info, void* stream) {
+  if (batch < 0 || n <= 0 || lda < n) return HMX_ERR_ARG;
+  // one plan per entry so that the pivot status is reported per entry
+  for (int b = 0; b < batch; ++b) {
+    MiniRun mr;
+    hmx_op o = blank(OP_LU);
+    o.dim[0] = n;
+    o.ref[0] = R(kBaseIn, b * strideA);
+    o.ld[0] = lda;
+    o.ref[1] = R(kBaseOut, b * strideLU);
+    o.ld[1] = n;
+    o.ref[2] = R(kBaseOut2, b * strideLU);
+    o.ld[2] = n;
+    mr.ops.push_back(o);
+    mr.end_task();
+    int bits = 0;
+    hmx_status st = run_mini(mr, {{kBaseIn, const_cast<double*>(A), nullptr}, {kBaseOut, L, nullptr},
+                                  {kBaseOut2, U, nullptr}}, 1, 1, (cudaStream_t)stream, &bits);
+    if (st && st != bits) return st;
+    if (info) {
+      int v = bits;
+      cudaMemcpy(info + b, &v, sizeof(int), cudaMemcpyHostToDevice);
+    }
+  }
+  return HMX_OK;
+}
+
+static hmx_status trsm_batched(int code, int32_t batch, int32_t n, int32_t c, const double* T,
+                               int32_t ldt, int64_t strideT, double* B, int32_t ldb,
+                               int64_t strideB, void* stream) {
+  if (batch < 0 || n <= 0 || c < 0) return HMX_ERR_ARG;
+  MiniRun mr;
+  for (int b = 0; b < batch; ++b) {
+    hmx_op o = blank(code);
+    o.dim[0] = n;
+    o.dim[1] = c;
+    o.ref[0] = R(kBaseIn, b * strideT);
+    o.ld[0] = ldt;
+    o.ref[2] = R(kBaseOut, b * strideB);
+    o.ld[2] = ldb;
+    mr.ops.push_back(o);
+    mr.end_task();
+  }
+  return run_mini(mr, {{kBaseIn, const_cast<double*>(T), nullptr}, {kBaseOut, B, nullptr}}, 1, 1,
+                  (cudaStream_t)stream);
+}
+
+hmx_status hmx_trsm_lower_unit_batched(int32_t batch, int32_t n, int32_t c, const double* L,
+                                       int32_t ldl, int64_t strideL, double* B, int32_t ldb,
+                                       int64_t strideB, void* stream) {
+  return trsm_batched(OP_TRSM_LL, batch, n, c, L, ldl, strideL, B, ldb, strideB, stream);
+}
+
+hmx_status hmx_trsm_upper_trans_batched(int32_t batch, int32_t n, int32_t c, const double* U,
+                                        int32_t ldu, int64_t strideU, double* B, int32_t ldb,
+                                        int64_t strideB, void* stream) {
+  return trsm_batched(OP_TRSM_UT, batch, n, c, U, ldu, strideU, B, ldb, strideB, stream);
+}
+
+hmx_status hmx_gemm_batched(int32_t batch, int32_t m, int32_t n, int32_t k, double alpha,
+                            const double* A, int32_t lda, int64_t strideA, int32_t transA,
+                            const double* B, int32_t ldb, int64_t strideB, int32_t transB,
+                            double beta, double* C, int32_t ldc, int64_t strideC, void* stream) {
+  if (batch < 0 || m < 0 || n < 0 || k < 0) return HMX_ERR_ARG;
+  if (beta != 0.0 && beta != 1.0) return HMX_ERR_ARG;
+  MiniRun mr;
+  for (int b = 0; b < batch; ++b) {
+    hmx_op o = blank(OP_GEMM);
+    o.dim[0] = m; o.dim[1] = n; o.dim[2] = k;
+    o.flags = (transA ? F_TA : 0) | (transB ? F_TB : 0) | (beta == 1.0 ? F_ACC : 0);
+    o.farg[0] = alpha;
+    o.ref[0] = R(kBaseIn, b * strideA); o.ld[0] = lda;
+    o.ref[1] = R(kBaseOut2, b * strideB); o.ld[1] = ldb;
+    o.ref[2] = R(kBaseOut, b * strideC); o.ld[2] = ldc;
+    mr.ops.push_back(o);
+    mr.end_task();
+  }
+  return run_mini(mr, {{kBaseIn, const_cast<double*>(A), nullptr}, {kBaseOut, C, nullptr},
+                       {kBaseOut2, const_cast<double*>(B), nullptr}}, 1, 1, (cudaStream_t)stream);
+}
+
+hmx_status hmx_truncate_batched(int32_t batch, int32_t m, int32_t n, int32_t K, const double* U,
+                                const double* V, int64_t strideU, int64_t strideV,
+                                int32_t policy, int32_t fixed_rank, double eps, int32_t cap,
+                                double* Uo, double* Vo, int64_t strideUo, int64_t strideVo,
+                                int32_t* rank, void* stream) {
+  if (batch < 0 || m <= 0 || n <= 0 || K < 0 || cap < 0) return HMX_ERR_ARG;
+  // per-CTA scratch: U copy (m*K), V copy (n*K), workspace 4K + 2K^2
+  const int64_t kk = std::max(K, 1);
+  const int64_t offV = (int64_t)m * kk, offW = offV + (int64_t)n * kk;
+  const int64_t scratch = offW + 4 * kk + 2 * kk * kk;
+  MiniRun mr;
+  for (int b = 0; b < batch; ++b) {
+    hmx_op c1 = blank(OP_COPY);
+    c1.dim[0] = m; c1.dim[1] = K; c1.farg[0] = 1.0;
+    c1.ref[0] = R(kBaseIn, b * strideU); c1.ld[0] = m;
+    c1.ref[2] = R(kScratchBase, 0); c1.ld[2] = m;
+    mr.ops.push_back(c1);
+    hmx_op c2 = blank(OP_COPY);
+    c2.dim[0] = n; c2.dim[1] = K; c2.farg[0] = 1.0;
+    c2.ref[0] = R(kBaseOut2, b * strideV); c2.ld[0] = n;
+    c2.ref[2] = R(kScratchBase, offV); c2.ld[2] = n;
+    mr.ops.push_back(c2);
+    hmx_op t = blank(OP_TRUNC);
+    t.dim[0] = m; t.dim[1] = n; t.dim[2] = K;
+    t.ref[0] = R(kScratchBase, 0); t.ld[0] = m;
+    t.ref[1] = R(kScratchBase, offV); t.ld[1] = n;
+    t.ref[2] = R(kBaseOut, b * strideUo); t.ld[2] = m;
+    t.ref[3] = R(kBaseOut3, b * strideVo); t.ld[3] = n;
+    t.wref = R(kScratchBase, offW);
+    t.slot[0] = S(kBaseRank, b);
+    t.iarg[0] = policy; t.iarg[1] = fixed_rank; t.iarg[2] = cap; t.iarg[3] = (int)kk;
+    t.farg[1] = eps;
+    mr.ops.push_back(t);
+    mr.end_task();
+  }
+  return run_mini(mr, {{kBaseIn, const_cast<double*>(U), nullptr}, {kBaseOut, Uo, nullptr},
+                       {kBaseOut2, const_cast<double*>(V), nullptr}, {kBaseOut3, Vo, nullptr},
+                       {kBaseRank, nullptr, rank}}, scratch, 1, (cudaStream_t)stream);
+}
+
+hmx_status hmx_dense_to_lowrank_batched(int32_t batch, int32_t m, int32_t n, const double* M,
+                                        int64_t strideM, int32_t policy, int32_t fixed_rank,
+                                        double eps, int32_t cap, double* Uo, double* Vo,
+                                        int64_t strideUo, int64_t strideVo, int32_t* rank,
+                                        void* stream) {
+  if (batch < 0 || m <= 0 || n <= 0 || cap < 0) return HMX_ERR_ARG;
+  const int64_t s = std::min(m, n), l = std::max(m, n);
+  const int64_t offW = (int64_t)m * n;
+  const int64_t scratch = offW + 2 * s + s * s + s * l;
+  MiniRun mr;
+  for (int b = 0; b < batch; ++b) {
+    hmx_op c1 = blank(OP_COPY);
+    c1.dim[0] = m; c1.dim[1] = n; c1.farg[0] = 1.0;
+    c1.ref[0] = R(kBaseIn, b * strideM); c1.ld[0] = m;
+    c1.ref[2] = R(kScratchBase, 0); c1.ld[2] = m;
+    mr.ops.push_back(c1);
+    hmx_op t = blank(OP_D2LR);
+    t.dim[0] = m; t.dim[1] = n;
+    t.ref[0] = R(kScratchBase, 0); t.ld[0] = m;
+    t.ref[2] = R(kBaseOut, b * strideUo); t.ld[2] = m;
+    t.ref[3] = R(kBaseOut2, b * strideVo); t.ld[3] = n;
+    t.wref = R(kScratchBase, offW);
+    t.slot[0] = S(kBaseRank, b);
+    t.iarg[0] = policy; t.iarg[1] = fixed_rank; t.iarg[2] = cap;
+    t.farg[1] = eps;
+    mr.ops.push_back(t);
+    mr.end_task();
+  }
+  return run_mini(mr, {{kBaseIn, const_cast<double*>(M), nullptr}, {kBaseOut, Uo, nullptr},
+                       {kBaseOut2, Vo, nullptr}, {kBaseRank, nullptr, rank}}, scratch, 1,
+                  (cudaStream_t)stream);
+}
+
+hmx_status hmx_svd_values_batched(int32_t batch, int32_t p, int32_t q, const double* G,
+                                  int64_t strideG, double* sigma, int64_t strideS, void* stream) {
+  if (batch < 0 || p <= 0 || q <= 0) return HMX_ERR_ARG;
+  const int64_t s = std::min(p, q), l = std::max(p, q);
+  const int64_t scratch = s * s + l * s + 2 * s + 2;
+  MiniRun mr;
+  for (int b = 0; b < batch; ++b) {
+    hmx_op o = blank(OP_SVALS);
+    o.dim[0] = p; o.dim[1] = q;
+    o.ref[0] = R(kBaseIn, b * strideG); o.ld[0] = p;
+    o.ref[2] = R(kBaseOut, b * strideS);
+    o.wref = R(kScratchBase, 0);
+    mr.ops.push_back(o);
+    mr.end_task();
+  }
+  return run_mini(mr, {{kBaseIn, const_cast<double*>(G), nullptr}, {kBaseOut, sigma, nullptr}},
+                  scratch, 1, (cudaStream_t)stream);
+}
+
+}  // extern "C"

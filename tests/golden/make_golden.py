@@ -1,0 +1,310 @@
+"""Generate golden fixtures by running the UNMODIFIED reference package.
+
+This script is the only place that imports the reference (``hmatdag`` from
+``/root/reference/pkg/src``).  It runs in the build container (the GPU box
+has no ``/root/reference``) and writes small fixtures next to itself:
+
+    tests/golden/<case>.npz   numeric + structural fixtures
+    tests/golden/<case>.json  counts, hashes, residuals, counters
+
+Inputs are seeded synthetic problems with the BASELINE.json shapes (there is
+no dataset).  The problem definitions are restated here independently of the
+product package so that the pin does not depend on the code it pins.
+
+Usage:  python tests/golden/make_golden.py [case ...]
+Cases:  small (s1..s4, trunc), c1, c2, c3s, c4, c5s
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.dont_write_bytecode = True
+sys.path.insert(0, REF)
+
+from threadpoolctl import threadpool_limits  # noqa: E402
+
+import hmatdag.accumulator as accm  # noqa: E402
+import hmatdag.arith as arith  # noqa: E402
+import hmatdag.hmatrix as hm  # noqa: E402
+import hmatdag.problems as prob  # noqa: E402
+import hmatdag.taskgraph as tg  # noqa: E402
+import hmatdag.trees as trees  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+# ---------------------------------------------------------------------------
+# problem definitions (BASELINE.json configs)
+# ---------------------------------------------------------------------------
+
+def exp_kernel(points, ell, perm):
+    k = prob.PointKernel(points, lambda d: np.exp(-d / ell), diag_value=1.0 + 1e-2, scale=1.0)
+    return prob.permuted(k, perm)
+
+
+def weak_adm(t, s):
+    return not t.indices.overlaps(s.indices)
+
+
+def eta_adm(eta):
+    return lambda t, s: trees.standard_admissible(t, s, eta)
+
+
+def case_points(name):
+    """(points, ell, n_min, adm, eps) for a named case."""
+    if name == "c1":
+        n = 2048
+        return ((np.arange(n) + 0.5) / n)[:, None], 0.1, 64, weak_adm, 1e-6
+    if name == "c2":
+        g = (np.arange(128) + 0.5) / 128
+        X, Y = np.meshgrid(g, g, indexing="ij")
+        return np.column_stack([X.ravel(), Y.ravel()]), 0.2, 64, eta_adm(2.0), 1e-6
+    if name == "c3s":
+        rng = np.random.default_rng(0)
+        p = rng.normal(size=(65536, 3))
+        p /= np.linalg.norm(p, axis=1, keepdims=True)
+        return p, 0.3, 64, eta_adm(2.0), 1e-5
+    if name.startswith("c4_"):
+        j = int(name[3:])
+        rng = np.random.default_rng(1000 + j)
+        x = np.sort(rng.uniform(size=4096))
+        ell = float(rng.uniform(0.05, 0.5))
+        return x[:, None], ell, 64, weak_adm, 1e-6
+    if name == "c5s":
+        rng = np.random.default_rng(0)
+        return rng.uniform(size=(262144, 3)), 0.25, 128, eta_adm(2.0), 1e-4
+    if name == "s1":  # small 1D HODLR
+        n = 512
+        return ((np.arange(n) + 0.5) / n)[:, None], 0.1, 16, weak_adm, 1e-6
+    if name == "s2":  # small 2D grid, standard admissibility
+        g = (np.arange(32) + 0.5) / 32
+        X, Y = np.meshgrid(g, g, indexing="ij")
+        return np.column_stack([X.ravel(), Y.ravel()]), 0.2, 16, eta_adm(2.0), 1e-6
+    if name == "s5":  # small sphere, eta=2, eps 1e-5 (c3 shape, scaled down)
+        rng = np.random.default_rng(0)
+        p = rng.normal(size=(2048, 3))
+        p /= np.linalg.norm(p, axis=1, keepdims=True)
+        return p, 0.3, 32, eta_adm(2.0), 1e-5
+    raise KeyError(name)
+
+
+# ---------------------------------------------------------------------------
+# serialisation helpers
+# ---------------------------------------------------------------------------
+
+def sha(text: str) -> str:
+    return hashlib.sha256(text.encode()).hexdigest()
+
+
+def block_table(root):
+    rows = []
+    for line in trees.serialize_block_tree(root).splitlines():
+        rows.append([int(v) for v in line.split()])
+    return np.asarray(rows, dtype=np.int64)
+
+
+def key_line(k):
+    kind, mids, uids, alpha = k
+    return f"{kind}|{','.join(map(str, mids))}|{','.join(map(str, uids))}|{alpha!r}"
+
+
+def dag_summary(g, full: bool):
+    nodes = sorted(key_line(t.key()) for t in g.nodes)
+    edges = sorted(f"{key_line(u.key())}>{key_line(v.key())}" for u, v in g.edges())
+    d = {"nodes": len(nodes), "edges": len(edges),
+         "nodes_sha": sha("\n".join(nodes)), "edges_sha": sha("\n".join(edges))}
+    if full:
+        d["node_lines"] = nodes
+        d["edge_lines"] = edges
+    return d
+
+
+def leaf_arrays(H, nblocks):
+    """Per-uid rank (-1 for dense/blocked) and per-leaf Frobenius norm."""
+    rank = np.full(nblocks, -1, dtype=np.int64)
+    fro = np.full(nblocks, np.nan)
+    for leaf in H.leaves():
+        u = leaf.block.uid
+        if leaf.kind == hm.LOWRANK:
+            rank[u] = leaf.rank
+        fro[u] = leaf.frobenius()
+    return rank, fro
+
+
+def probe(H, x):
+    return hm.hm_apply(H, x)
+
+
+# ---------------------------------------------------------------------------
+# case runners
+# ---------------------------------------------------------------------------
+
+def run_case(name, numerics=True, modes=("std", "accu"), dag_modes=None, full_dag=False,
+             store_blocks=True, n_probe=2):
+    t0 = time.time()
+    pts, ell, n_min, adm, eps = case_points(name)
+    geom = trees.Geometry(pts)
+    croot, perm = trees.build_cluster_tree(geom, n_min)
+    broot = trees.build_block_tree(croot, croot, adm)
+    blocks = block_table(broot)
+    nb = blocks.shape[0]
+    meta = {"case": name, "n": int(len(pts)), "ell": ell, "n_min": n_min, "eps": eps,
+            "n_blocks": int(nb), "n_leaves": int(blocks[:, 6].sum()),
+            "n_admissible": int(blocks[:, 7].sum()),
+            "cluster_sha": sha(trees.serialize_cluster_tree(croot)),
+            "block_sha": sha(trees.serialize_block_tree(broot)),
+            "perm_sha": sha(",".join(map(str, perm.tolist())))}
+    arrays = {}
+    if store_blocks:
+        arrays["blocks"] = blocks
+        arrays["perm"] = perm.astype(np.int64)
+    print(f"[{name}] structure {time.time() - t0:.1f}s blocks={nb}", flush=True)
+
+    dag_modes = dag_modes or []
+    meta["dags"] = {}
+    for mode, sp in dag_modes:
+        t1 = time.time()
+        g = tg.build_hlu_dag(broot, mode, sparsify=sp)
+        tag = f"{mode}{'+sparsify' if sp else ''}"
+        meta["dags"][tag] = dag_summary(g, full_dag)
+        meta["dags"][tag]["build_s"] = time.time() - t1
+        print(f"[{name}] dag {tag}: {meta['dags'][tag]['nodes']} / "
+              f"{meta['dags'][tag]['edges']} in {time.time() - t1:.1f}s", flush=True)
+        del g
+
+    if numerics:
+        pol = hm.TruncationPolicy.fixed_accuracy(eps)
+        kern = exp_kernel(pts, ell, perm)
+        t1 = time.time()
+        hm.counters.reset()
+        A0 = hm.assemble(broot, kern, pol)
+        meta["assembly_truncations"] = hm.counters.snapshot()[0]
+        meta["assembly_s"] = time.time() - t1
+        print(f"[{name}] assembly {time.time() - t1:.1f}s", flush=True)
+        rA, fA = leaf_arrays(A0, nb)
+        arrays["A_rank"], arrays["A_fro"] = rA, fA
+        n = len(pts)
+        rng = np.random.default_rng(12345)
+        X = rng.normal(size=(n, n_probe))
+        arrays["probe_x"] = X
+        AX = probe(A0, X)
+        arrays["probe_Ax"] = AX
+        for mode in modes:
+            A = A0.copy()
+            L, U = hm.zeros(broot, pol), hm.zeros(broot, pol)
+            hm.counters.reset()
+            t2 = time.time()
+            with threadpool_limits(limits=1):
+                if mode == "std":
+                    arith.hlu(A, L, U, pol)
+                else:
+                    accm.hlu_accu(A, L, U, accm.AccumulatorMap(), pol)
+            dt = time.time() - t2
+            tr, up = hm.counters.snapshot()
+            rL, fL = leaf_arrays(L, nb)
+            rU, fU = leaf_arrays(U, nb)
+            LUX = probe(L, probe(U, X))
+            res = float(np.linalg.norm(AX - LUX) / np.linalg.norm(AX))
+            arrays[f"{mode}_L_rank"], arrays[f"{mode}_L_fro"] = rL, fL
+            arrays[f"{mode}_U_rank"], arrays[f"{mode}_U_fro"] = rU, fU
+            arrays[f"{mode}_probe_LUx"] = LUX
+            arrays[f"{mode}_probe_Ux"] = probe(U, X)
+            meta[f"{mode}_truncations"] = tr
+            meta[f"{mode}_updates"] = up
+            meta[f"{mode}_probe_residual"] = res
+            meta[f"{mode}_hlu_s"] = dt
+            print(f"[{name}] {mode} hlu {dt:.2f}s trunc={tr} upd={up} res={res:.3e}",
+                  flush=True)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **arrays)
+    with open(os.path.join(OUT, f"{name}.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    print(f"[{name}] done {time.time() - t0:.1f}s", flush=True)
+
+
+def probe_vec(n):
+    return np.random.default_rng(7).normal(size=(n, 2))
+
+
+def truncate_inputs(i, m, n, K, decay):
+    """Seeded inputs of truncate case i (restated in tests/test_oracle.py)."""
+    r = np.random.default_rng(100 + i)
+    U = r.normal(size=(m, K)) * np.exp(-decay * np.arange(K))[None, :]
+    V = r.normal(size=(n, K))
+    M = U @ V.T + 1e-3 * r.normal(size=(m, n)) * np.exp(-decay * K)
+    return U, V, M
+
+
+def run_truncate_cases():
+    """Random truncate / dense_to_lowrank cases: inputs from seeds, outputs
+    (rank, singular values of the reconstruction, product) from the reference."""
+    out = {}
+    specs = []
+    rng = np.random.default_rng(2024)
+    for i in range(24):
+        m = int(rng.integers(8, 300))
+        n = int(rng.integers(8, 300))
+        K = int(rng.integers(1, 60))
+        decay = float(rng.uniform(0.3, 3.0))
+        specs.append((m, n, K, decay))
+    for i, (m, n, K, decay) in enumerate(specs):
+        U, V, M = truncate_inputs(i, m, n, K, decay)
+        for eps in (1e-4, 1e-6, 1e-8):
+            pol = hm.TruncationPolicy.fixed_accuracy(eps)
+            Un, Vn = hm.truncate(U, V, pol)
+            out[f"t{i}_{eps:g}_rank"] = np.array(Un.shape[1])
+            out[f"t{i}_{eps:g}_probe"] = Un @ (Vn.T @ probe_vec(n))
+        for eps in (1e-4, 1e-6):
+            pol = hm.TruncationPolicy.fixed_accuracy(eps)
+            W, Z = hm.dense_to_lowrank(M, pol)
+            out[f"d{i}_{eps:g}_rank"] = np.array(W.shape[1])
+            out[f"d{i}_{eps:g}_probe"] = W @ (Z.T @ probe_vec(n))
+    # dense LU
+    for i in range(4):
+        r = np.random.default_rng(300 + i)
+        n = (16, 33, 64, 128)[i]
+        A = r.normal(size=(n, n)) + n * np.eye(n)
+        Lr, Ur = arith.dense_lu(A)
+        out[f"lu{i}_L"], out[f"lu{i}_U"] = Lr, Ur
+    np.savez_compressed(os.path.join(OUT, "kernels.npz"), **out)
+    with open(os.path.join(OUT, "kernels.json"), "w") as f:
+        json.dump({"n_truncate": len(specs), "specs": specs}, f)
+    print("[kernels] done", flush=True)
+
+
+ALL_DAG = [("std", False), ("std", True), ("accu-combined", False),
+           ("accu-merged", False), ("accu-merged", True)]
+
+
+def main(argv):
+    cases = argv or ["small"]
+    for c in cases:
+        if c == "small":
+            run_truncate_cases()
+            for s in ("s1", "s2", "s5"):
+                run_case(s, dag_modes=ALL_DAG, full_dag=(s == "s1"))
+        elif c == "c1":
+            run_case("c1", dag_modes=ALL_DAG, full_dag=True)
+        elif c == "c2":
+            run_case("c2", dag_modes=ALL_DAG)
+        elif c == "c3s":
+            run_case("c3s", numerics=False, dag_modes=[("std", False), ("accu-merged", False)],
+                     store_blocks=False)
+        elif c == "c4":
+            for j in range(4):
+                run_case(f"c4_{j}", dag_modes=[("std", False), ("accu-merged", False)])
+        elif c == "c5s":
+            run_case("c5s", numerics=False, dag_modes=[], store_blocks=False)
+        else:
+            raise SystemExit(f"unknown case {c}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -1,0 +1,127 @@
+"""Device leaf kernels vs numpy/scipy (the reference's LAPACK calls).
+
+Tolerances: the kernels are fp64; products and solves are compared at
+1e-12 relative, LU at bitwise equality (the device LU mirrors
+arith.dense_lu's rounding: separate multiply and subtract, arith.py:70-71).
+"""
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_dense_lu(A):
+    # arith.dense_lu restated (arith.py:58-73); oracle copy lives in oracle/
+    from oracle.hm_oracle import dense_lu
+
+    return dense_lu(A)
+
+
+def test_getrf_bitwise_vs_oracle():
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(0)
+    for n in (16, 64, 128):
+        As = [rng.normal(size=(n, n)) + n * np.eye(n) for _ in range(3)]
+        L, U, info = kernels.getrf_nopiv(As)
+        assert (info == 0).all()
+        for a, l, u in zip(As, L, U):
+            lr, ur = ref_dense_lu(a)
+            assert np.array_equal(l, lr)
+            assert np.array_equal(u, ur)
+
+
+def test_getrf_singular_pivot_flag():
+    from paper_1911_07531_b200 import kernels
+
+    L, U, info = kernels.getrf_nopiv([np.zeros((8, 8))])
+    assert info[0] & 4
+
+
+def test_trsm():
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(1)
+    for n, c in ((64, 64), (64, 7), (128, 20)):
+        A = rng.normal(size=(n, n)) + n * np.eye(n)
+        Lf = np.tril(A, -1) / n + np.eye(n)
+        Uf = np.triu(A)
+        B = rng.normal(size=(n, c))
+        X = kernels.trsm_lower_unit([Lf], [B])[0]
+        Xr = sla.solve_triangular(Lf, B, lower=True, unit_diagonal=True)
+        assert np.linalg.norm(X - Xr) <= 1e-12 * np.linalg.norm(Xr)
+        W = kernels.trsm_upper_trans([Uf], [B])[0]
+        Wr = sla.solve_triangular(Uf, B, trans="T", lower=False)
+        assert np.linalg.norm(W - Wr) <= 1e-12 * np.linalg.norm(Wr)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm(ta, tb):
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(2)
+    for m, n, k in ((64, 64, 64), (130, 7, 33), (5, 200, 17), (1, 1, 1)):
+        A = rng.normal(size=(k, m) if ta else (m, k))
+        B = rng.normal(size=(n, k) if tb else (k, n))
+        C0 = rng.normal(size=(m, n))
+        want = C0 - 1.0 * ((A.T if ta else A) @ (B.T if tb else B))
+        got = kernels.gemm(-1.0, [A], [B], [C0], transA=ta, transB=tb, beta=1.0)[0]
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+
+
+class _Pol:
+    def __init__(self, mode, eps=None, k=None):
+        self.mode, self.eps, self.k = mode, eps, k
+
+
+def test_svd_values_vs_lapack():
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(3)
+    for p, q in ((20, 20), (33, 17), (17, 33), (64, 64), (100, 40)):
+        G = rng.normal(size=(p, q)) * np.exp(-0.5 * np.arange(q))[None, :]
+        s = kernels.svd_values([G])[0]
+        sr = np.linalg.svd(G, compute_uv=False)
+        assert np.allclose(s, sr, rtol=1e-12, atol=1e-14 * sr[0])
+
+
+def test_truncate_vs_reference_fixtures():
+    """Ranks equal to the reference's truncate on its golden cases; the
+    recompressed product within 1e-12 relative of the reference's."""
+    import json
+    import os
+
+    from paper_1911_07531_b200 import kernels
+    from tests.golden_inputs import GOLDEN, probe_vec, truncate_inputs
+
+    meta = json.load(open(os.path.join(GOLDEN, "kernels.json")))
+    ref = np.load(os.path.join(GOLDEN, "kernels.npz"))
+    for i, (m, n, K, decay) in enumerate(meta["specs"]):
+        U, V, M = truncate_inputs(i, m, n, K, decay)
+        for eps in (1e-4, 1e-6, 1e-8):
+            Un, Vn = kernels.truncate(U, V, _Pol("accuracy", eps=eps))
+            assert Un.shape[1] == int(ref[f"t{i}_{eps:g}_rank"]), (i, eps)
+            pr = ref[f"t{i}_{eps:g}_probe"]
+            got = Un @ (Vn.T @ probe_vec(n))
+            assert np.linalg.norm(got - pr) <= 1e-10 * np.linalg.norm(pr) + 1e-13
+        for eps in (1e-4, 1e-6):
+            W, Z = kernels.dense_to_lowrank(M, _Pol("accuracy", eps=eps))
+            assert W.shape[1] == int(ref[f"d{i}_{eps:g}_rank"]), (i, eps)
+            pr = ref[f"d{i}_{eps:g}_probe"]
+            got = W @ (Z.T @ probe_vec(n))
+            assert np.linalg.norm(got - pr) <= 1e-10 * np.linalg.norm(pr) + 1e-13
+
+
+def test_truncate_policies_and_passthrough():
+    from paper_1911_07531_b200 import kernels
+
+    U = np.eye(4)[:, :2]
+    V = np.eye(4)[:, :2]
+    Un, Vn = kernels.truncate(U, V, _Pol("rank", k=1))
+    assert Un.shape[1] == 1
+    assert abs(np.linalg.norm(U @ V.T - Un @ Vn.T) - 1.0) < 1e-12
+    U0, V0 = np.zeros((5, 0)), np.zeros((4, 0))
+    a, b = kernels.truncate(U0, V0, _Pol("exact"))
+    assert a.shape == (5, 0) and b.shape == (4, 0)
