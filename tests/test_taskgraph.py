@@ -1,0 +1,107 @@
+"""DAG parity: the product's refinement builder vs the reference's DAGs.
+
+Node and edge sets are compared through the sha256 of their sorted
+canonical lines (fixture format of tests/golden/make_golden.py, which ran
+the reference's build_hlu_dag); small cases also compare the full lists.
+"""
+
+import hashlib
+
+import pytest
+
+from paper_1911_07531_b200 import configs, taskgraph as tg
+from paper_1911_07531_b200.trees import BlockTable, serialize_block_tree, serialize_cluster_tree
+from tests.golden_inputs import have, load
+
+VARIANTS = [("std", False), ("std", True), ("accu-combined", False), ("accu-merged", False),
+            ("accu-merged", True)]
+
+
+def _sha(s):
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["s1", "s2", "s5", "c1", "c2", "c4_0"])
+def test_trees_match_reference(name):
+    if not have(name):
+        pytest.skip("fixture missing")
+    meta, arr = load(name)
+    cfg = configs.config(name)
+    geom, root, perm, broot = configs.structure(cfg)
+    assert _sha(serialize_cluster_tree(root)) == meta["cluster_sha"]
+    assert _sha(serialize_block_tree(broot)) == meta["block_sha"]
+    assert _sha(",".join(map(str, perm.tolist()))) == meta["perm_sha"]
+
+
+@pytest.mark.parametrize("name", ["s1", "c1", "s2", "c4_0"])
+def test_dags_match_reference(name):
+    if not have(name):
+        pytest.skip("fixture missing")
+    meta, _ = load(name)
+    cfg = configs.config(name)
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    for mode, sp in VARIANTS:
+        tag = f"{mode}{'+sparsify' if sp else ''}"
+        if tag not in meta["dags"]:
+            continue
+        ref = meta["dags"][tag]
+        g = tg.build_hlu_dag(bt, mode, sparsify=sp)
+        assert g.stats() == (ref["nodes"], ref["edges"]), tag
+        nh, eh = tg.canonical_hashes(g)
+        if "node_lines" in ref:
+            assert sorted(tg.key_line(t.key()) for t in g.nodes) == ref["node_lines"]
+        assert nh == ref["nodes_sha"], tag
+        assert eh == ref["edges_sha"], tag
+        assert tg.check_acyclic(g)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["s5", "c2"])
+def test_dags_match_reference_large(name):
+    test_dags_match_reference(name)
+
+
+def test_fig2_micro_dag():
+    """2x2 single refinement: 5 nodes, 5 edges 0->1, 0->2, 1->3, 2->3, 3->4."""
+    import numpy as np
+
+    from paper_1911_07531_b200.trees import Geometry, build_block_tree, build_cluster_tree
+
+    root, _ = build_cluster_tree(Geometry(np.arange(4.0)[:, None]), 2)
+    b = build_block_tree(root, root, lambda t, s: False)
+    g = tg.build_hlu_dag(b, "std")
+    assert g.stats() == (5, 5)
+    pos = {id(t): i for i, t in enumerate(g.nodes)}
+    edges = sorted((pos[id(u)], pos[id(v)]) for u, v in g.edges())
+    assert edges == [(0, 1), (0, 2), (1, 3), (2, 3), (3, 4)]
+
+
+def test_sparsify_preserves_closure_and_modes():
+    cfg = configs.config("s1")
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    g0 = tg.build_hlu_dag(bt, "std")
+    g1 = tg.build_hlu_dag(bt, "std", sparsify=True)
+    assert g1.n_edges < g0.n_edges
+    assert tg.transitive_closure(g0) == tg.transitive_closure(g1)
+    with pytest.raises(ValueError):
+        tg.build_hlu_dag(bt, "accu-combined", sparsify=True)
+    with pytest.raises(ValueError):
+        tg.build_hlu_dag(bt, "bogus")
+    g2 = tg.build_hlu_dag(bt, "std", workers=4, chunk_size=2)
+    assert tg.canonical_hashes(g2) == tg.canonical_hashes(g0)
+    dot = tg.to_dot(g0)
+    assert dot.startswith("digraph") and dot.count("->") == g0.n_edges
+
+
+def test_levels_and_csr():
+    cfg = configs.config("s1")
+    _, _, _, broot = configs.structure(cfg)
+    g = tg.build_hlu_dag(BlockTable(broot), "accu-merged")
+    ptr, idx = g.csr()
+    assert ptr[-1] == g.n_edges
+    lv = g.levels()
+    for i in range(g.n_nodes):
+        for j in idx[ptr[i]:ptr[i + 1]]:
+            assert lv[j] > lv[i]
