@@ -1,0 +1,86 @@
+"""Standard H-arithmetic on the GPU (drop-in for hmatdag.arith, arith.py:1-140).
+
+``hlu(A, L, U, policy)`` factors A = L U (unpivoted, L unit lower) by
+executing the lowered task DAG of taskgraph.build_hlu_dag on the device;
+A is consumed as workspace, L and U (from ``zeros``) receive the factors,
+exactly like the reference.  The result is the one of the sequential
+recursion ``arith.hlu`` (same tasks, same truncation sequence): std-mode
+DAG execution is order independent.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import engine
+from .hmatrix import HMatrix, TruncationPolicy, counters
+
+PIVOT_CUTOFF = 1e-14
+
+
+class SingularPivotError(RuntimeError):
+    pass
+
+
+_PLANS = {}
+
+
+def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0):
+    """Cached execution plan (planning and upload happen once per tree)."""
+    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas)
+    p = _PLANS.get(key)
+    if p is None or p.table is not table:
+        p = engine.ExecPlan(table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify,
+                            max_ctas=max_ctas)
+        _PLANS[key] = p
+    return p
+
+
+def clear_plans():
+    _PLANS.clear()
+
+
+def _check_operands(*ms):
+    t = ms[0].table
+    for M in ms:
+        if not isinstance(M, HMatrix):
+            raise TypeError("operands must be device HMatrix views")
+        if M.table is not t:
+            raise ValueError("non-conformal operands (different block trees)")
+        if M.uid != ms[0].uid:
+            raise ValueError("non-conformal operands (different blocks)")
+    if ms[0].uid != 0:
+        raise NotImplementedError("factorization of a sub-block view: factor the root")
+    return t
+
+
+def run_hlu(A, L, U, policy, mode, exec_mode=engine.EXEC_PERSISTENT, dag_mode=None,
+            sparsify=False, stream=None):
+    t = _check_operands(A, L, U)
+    rc = A.store.layout.rank_cap
+    for M in (L, U):
+        if M.store.layout.rank_cap != rc:
+            raise ValueError("L/U storage rank_cap differs from A's")
+    plan = get_plan(t, mode, policy, rc, dag_mode, sparsify)
+    plan.run(A.store, L.store, U.store, exec_mode, stream)
+    c = plan.counters(stream)
+    counters.add(c["truncations"], c["updates"])
+    return plan
+
+
+def hlu(A: HMatrix, L: HMatrix, U: HMatrix, policy: TruncationPolicy, **kw):
+    """Factor A = L U (arith.py:76-94); A is consumed as workspace."""
+    return run_hlu(A, L, U, policy, "std", **kw)
+
+
+def dense_lu(A: np.ndarray):
+    """Unpivoted LU of one dense block on the device (arith.py:58-73)."""
+    from . import kernels
+
+    A = np.asarray(A, dtype=float)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError("LU needs a square block")
+    Ls, Us, info = kernels.getrf_nopiv([A])
+    if info[0]:
+        raise SingularPivotError("vanishing pivot")
+    return Ls[0], Us[0]

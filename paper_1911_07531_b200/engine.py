@@ -1,0 +1,253 @@
+"""Device storage and DAG execution of H-arithmetic plans.
+
+``HStore``   one H-matrix in HBM: a pooled fp64 tensor holding every dense
+             leaf and every low-rank factor arena (Layout offsets) plus an
+             int32 rank array indexed by block uid.
+``ExecPlan`` a lowered H-LU (planner.Program) bound to its execution graph:
+             the node set is the reference DAG of taskgraph.build_hlu_dag;
+             edges are that DAG's edges plus, for accumulator modes, the
+             per-accumulator fold order of accumulator.hlu_accu (the DAG
+             alone does not order a parent shift against a direct add into
+             the same accumulator — SURVEY.md finding 3).  The graph is
+             uploaded once (CSR + in-degrees + ASAP wavefronts) into an
+             hmx_plan and replayed by the device executors.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from . import taskgraph as tg
+from .planner import ACC_BASE_ID, Layout, dataflow_edges, plan_hlu
+from .trees import BlockTable
+
+EXEC_WAVE, EXEC_GRAPH, EXEC_PERSISTENT, EXEC_SEQUENTIAL = 0, 1, 2, 3
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("the H-LU engine needs a CUDA device; there is no CPU fallback")
+    return torch
+
+
+class HStore:
+    """Device storage of one H-matrix (values pool + rank slots)."""
+
+    def __init__(self, layout: Layout, values=None, ranks=None):
+        torch = _torch()
+        self.layout = layout
+        self.table = layout.table
+        n = self.table.n
+        self.values = values if values is not None else torch.zeros(
+            layout.size, dtype=torch.float64, device="cuda")
+        if ranks is None:
+            r = np.full(n, -1, dtype=np.int32)
+            r[self.table.leaf & self.table.adm] = 0
+            ranks = torch.from_numpy(r).cuda()
+        self.ranks = ranks
+
+    def clone(self):
+        return HStore(self.layout, self.values.clone(), self.ranks.clone())
+
+    def copy_from(self, other: "HStore"):
+        self.values.copy_(other.values)
+        self.ranks.copy_(other.ranks)
+
+    # host transfers -----------------------------------------------------
+    def upload_leaves(self, leaves):
+        """leaves: uid -> ("D", M) | ("R", U, V) (row-major numpy)."""
+        torch = _torch()
+        lay, t = self.layout, self.table
+        buf = np.zeros(lay.size, dtype=np.float64)
+        r = np.full(t.n, -1, dtype=np.int32)
+        for u, x in leaves.items():
+            m, n = int(t.m[u]), int(t.nc[u])
+            if x[0] == "D":
+                o = int(lay.d_off[u])
+                buf[o:o + m * n] = np.asarray(x[1], dtype=np.float64).T.ravel()
+            else:
+                k = x[1].shape[1]
+                if k > lay.cap[u]:
+                    raise _lib.HmxError(_lib.HMX_ERR_RANK_OVERFLOW, f"upload of block {u}")
+                uo, vo = int(lay.u_off[u]), int(lay.v_off[u])
+                buf[uo:uo + m * k] = np.asarray(x[1]).T.ravel()
+                buf[vo:vo + n * k] = np.asarray(x[2]).T.ravel()
+                r[u] = k
+        self.values.copy_(torch.from_numpy(buf))
+        self.ranks.copy_(torch.from_numpy(r))
+
+    def upload_leaf(self, u, x):
+        torch = _torch()
+        lay, t = self.layout, self.table
+        m, n = int(t.m[u]), int(t.nc[u])
+        if x[0] == "D":
+            o = int(lay.d_off[u])
+            self.values[o:o + m * n].copy_(torch.from_numpy(np.ascontiguousarray(x[1].T).ravel()))
+        else:
+            k = x[1].shape[1]
+            if k > lay.cap[u]:
+                raise _lib.HmxError(_lib.HMX_ERR_RANK_OVERFLOW, f"upload of block {u}")
+            uo, vo = int(lay.u_off[u]), int(lay.v_off[u])
+            self.values[uo:uo + m * k].copy_(torch.from_numpy(np.ascontiguousarray(x[1].T).ravel()))
+            self.values[vo:vo + n * k].copy_(torch.from_numpy(np.ascontiguousarray(x[2].T).ravel()))
+            self.ranks[u] = k
+
+    def download_leaf(self, u):
+        lay, t = self.layout, self.table
+        m, n = int(t.m[u]), int(t.nc[u])
+        if t.adm[u]:
+            k = int(self.ranks[u].item())
+            uo, vo = int(lay.u_off[u]), int(lay.v_off[u])
+            U = self.values[uo:uo + m * k].cpu().numpy().reshape(k, m).T.copy()
+            V = self.values[vo:vo + n * k].cpu().numpy().reshape(k, n).T.copy()
+            return ("R", U, V)
+        o = int(lay.d_off[u])
+        return ("D", self.values[o:o + m * n].cpu().numpy().reshape(n, m).T.copy())
+
+    def download_leaves(self):
+        lay, t = self.layout, self.table
+        buf = self.values.cpu().numpy()
+        r = self.ranks.cpu().numpy()
+        out = {}
+        for u in t.leaves(0):
+            m, n = int(t.m[u]), int(t.nc[u])
+            if t.adm[u]:
+                k = int(r[u])
+                uo, vo = int(lay.u_off[u]), int(lay.v_off[u])
+                U = buf[uo:uo + m * k].reshape(k, m).T.copy()
+                V = buf[vo:vo + n * k].reshape(k, n).T.copy()
+                out[u] = ("R", U, V)
+            else:
+                o = int(lay.d_off[u])
+                out[u] = ("D", buf[o:o + m * n].reshape(n, m).T.copy())
+        return out
+
+
+class ExecPlan:
+    """Lowered H-LU plan + its device execution graph."""
+
+    def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
+                 sparsify=False, max_ctas=0):
+        if mode not in ("std", "accu"):
+            raise ValueError("mode must be 'std' or 'accu'")
+        self.table = table
+        self.mode = mode
+        self.policy = policy
+        self.rank_cap = rank_cap
+        prog = plan_hlu(table, mode, policy, rank_cap)
+        self.prog = prog
+        self.layout = prog.layout
+        dag_mode = dag_mode or ("std" if mode == "std" else tg.MERGED)
+        if (mode == "std") != (dag_mode == tg.STD):
+            raise ValueError(f"DAG mode {dag_mode} does not execute {mode} arithmetic")
+        if dag_mode == tg.COMBINED:
+            raise NotImplementedError("combined-mode execution: use accu-merged")
+        self.dag_mode = dag_mode
+        self.dag = tg.build_hlu_dag(table, dag_mode, sparsify=sparsify)
+        ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()
+        self.succ_ptr, self.succ_idx = ptr, idx
+        lv = tg.asap_levels(len(prog.keys), ptr, idx)
+        order = np.argsort(lv, kind="stable").astype(np.int32)
+        counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
+        self.levels = lv
+        self.wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        self.wave_tasks = order
+        self.n_tasks = len(prog.keys)
+        self.plan = _lib.Plan(prog.ops, prog.task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
+                              prog.scratch_doubles, prog.scratch_ranks, max_ctas)
+        torch = _torch()
+        self.acc_values = torch.zeros(prog.acc_size, dtype=torch.float64, device="cuda")
+        self.acc_ranks = torch.zeros(max(table.n, 1), dtype=torch.int32, device="cuda")
+        self.plan.bind(ACC_BASE_ID, self.acc_values, self.acc_ranks)
+
+    def _exec_graph(self):
+        """Successor CSR over program tasks (program order = trace order).
+
+        std: the reference DAG's edges (bit-exact node and edge sets; its
+        execution equals arith.hlu).
+        accu: the DAG's node set with edges from the data flow of
+        accumulator.hlu_accu.  The reference merged DAG orders add_upd tasks
+        on nested blocks by a WAW on matrix A although they write different
+        accumulators, and in places that order contradicts hlu_accu's
+        per-accumulator fold order; data-flow edges replay hlu_accu exactly.
+        """
+        prog = self.prog
+        pos = {}
+        for i, k in enumerate(prog.keys):
+            if k in pos:
+                raise RuntimeError(f"duplicate planned task {k}")
+            pos[k] = i
+        dag_to_prog = []
+        for t in self.dag.nodes:
+            k = (t.kind, t.uids, t.alpha)
+            if k not in pos:
+                raise RuntimeError(f"DAG task {k} has no lowered program")
+            dag_to_prog.append(pos[k])
+        if len(dag_to_prog) != len(pos):
+            raise RuntimeError("planned tasks and DAG nodes differ")
+        dptr, didx = self.dag.csr()
+        dag_edges = set()
+        for i in range(len(dag_to_prog)):
+            a = dag_to_prog[i]
+            for j in didx[dptr[i]:dptr[i + 1]]:
+                dag_edges.add((a, dag_to_prog[j]))
+        if self.mode == "std":
+            edges = dag_edges
+            n_extra = 0
+        else:
+            tables = {b: self.table for b in range(4)}
+            edges = dataflow_edges(prog, tables)
+            n_extra = len(edges - dag_edges)
+        self.n_dag_edges_kept = len(edges & dag_edges)
+        n = len(prog.keys)
+        src = np.fromiter((a for a, _ in edges), dtype=np.int64, count=len(edges))
+        dst = np.fromiter((b for _, b in edges), dtype=np.int64, count=len(edges))
+        if len(edges) and not (src < dst).all():
+            raise RuntimeError("execution graph contradicts program order")
+        o = np.lexsort((dst, src))
+        src, dst = src[o], dst[o]
+        ptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(ptr, src + 1, 1)
+        ptr = np.cumsum(ptr).astype(np.int32)
+        return ptr, dst.astype(np.int32), len(dag_edges), n_extra
+
+    def bind(self, A: HStore, L: HStore, U: HStore):
+        for i, s in enumerate((A, L, U)):
+            if s.layout.table is not self.table:
+                raise ValueError("operand is not over the plan's block tree")
+            if (s.layout.u_off != self.layout.u_off).any() or (s.layout.d_off != self.layout.d_off).any():
+                raise ValueError("operand storage layout differs from the plan's")
+            self.plan.bind(i, s.values, s.ranks)
+
+    def run(self, A: HStore, L: HStore, U: HStore, exec_mode=EXEC_PERSISTENT, stream=None,
+            check=True):
+        self.bind(A, L, U)
+        self.plan.reset_counters(stream)
+        self.plan.execute(exec_mode, stream)
+        if check:
+            self.check(stream)
+
+    def check(self, stream=None):
+        st = self.plan.status(stream)
+        if st:
+            if st & _lib.HMX_ERR_PIVOT:
+                from .arith import SingularPivotError
+
+                raise SingularPivotError("vanishing pivot in a diagonal leaf (device)")
+            raise _lib.HmxError(st, "H-LU execution")
+
+    def counters(self, stream=None):
+        c = self.plan.counters(stream)
+        return {"truncations": c[0], "flops": c[1], "bytes": c[2], "tasks": c[3],
+                "updates": self.prog.updates}
+
+    def stats(self):
+        w = np.diff(self.wave_ptr)
+        return {"tasks": self.n_tasks, "ops": int(len(self.prog.ops)), "dag_edges": self.n_dag_edges,
+                "exec_edges": int(len(self.succ_idx)), "dataflow_only_edges": self.n_chain_edges, "waves": int(len(w)),
+                "max_wave": int(w.max()) if len(w) else 0,
+                "scratch_mb_per_cta": self.prog.scratch_doubles * 8 / 2**20,
+                "acc_mb": self.prog.acc_size * 8 / 2**20, "pool_mb": self.layout.size * 8 / 2**20}

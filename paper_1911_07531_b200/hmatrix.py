@@ -1,0 +1,305 @@
+"""H-matrix storage, rank control and assembly (drop-in for hmatdag.hmatrix).
+
+An :class:`HMatrix` is a *view* of one block of a device-resident H-matrix
+(:class:`~.engine.HStore`): leaves live in a pooled fp64 HBM tensor
+(column-major dense leaves, U/V factor arenas with capacity ``rank_cap``)
+and ranks in an int32 device array.  The reference API is kept — ``kind``,
+``children``, ``D``/``U``/``V`` (host copies), ``rank``, ``to_dense``,
+``frobenius``, ``copy``, ``leaves``, ``set_lowrank``, ``child_offsets``
+(hmatrix.py:141-224) — but the arithmetic runs on the GPU through the
+planner/executor (arith.py, accumulator.py).
+
+Assembly (hmatrix.py:227-248) evaluates kernel blocks on the device
+(hmx_exp_kernel_blocks for the exponential point kernels of the BASELINE
+configs) and compresses admissible blocks: blocks with min(m, n) <= 128 by
+the device Jacobi SVD (the same op as dense_to_lowrank inside H-LU);
+larger blocks by a randomized range finder with power iteration on cuBLAS /
+cuSOLVER through torch, whose sample size grows until the trailing
+singular value of the sketch sits three decades below the cut — so ranks
+agree with LAPACK's dgesdd (tests/test_hlu_gpu.py checks the c1/c2 ranks
+against the reference fixtures).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .trees import Block, BlockTable
+
+ZERO_CUTOFF = 1e-14
+DENSE = "dense"
+LOWRANK = "lowrank"
+BLOCKED = "blocked"
+DEFAULT_RANK_CAP = 128
+
+
+class TruncationPolicy:
+    """Exact, FixedRank(k) or FixedAccuracy(eps) (hmatrix.py:36-78)."""
+
+    __slots__ = ("mode", "k", "eps")
+
+    def __init__(self, mode, k=None, eps=None):
+        self.mode = mode
+        self.k = k
+        self.eps = eps
+
+    @classmethod
+    def exact(cls):
+        return cls("exact")
+
+    @classmethod
+    def fixed_rank(cls, k: int):
+        if k < 0:
+            raise ValueError("rank must be >= 0")
+        return cls("rank", k=k)
+
+    @classmethod
+    def fixed_accuracy(cls, eps: float):
+        if eps <= 0:
+            raise ValueError("accuracy must be positive")
+        return cls("accuracy", eps=eps)
+
+    def keep(self, sigma: np.ndarray) -> int:
+        if sigma.size == 0 or sigma[0] <= 0.0:
+            return 0
+        if self.mode == "rank":
+            r = min(self.k, sigma.size)
+            return int(np.count_nonzero(sigma[:r] > ZERO_CUTOFF * sigma[0]))
+        cut = self.eps if self.mode == "accuracy" else ZERO_CUTOFF
+        return int(np.count_nonzero(sigma > cut * sigma[0]))
+
+    def __repr__(self):
+        if self.mode == "rank":
+            return f"FixedRank({self.k})"
+        if self.mode == "accuracy":
+            return f"FixedAccuracy({self.eps})"
+        return "Exact"
+
+
+EXACT = TruncationPolicy.exact()
+
+
+class OpCounters:
+    """Truncation / update counters (hmatrix.py:84-110), fed by the device."""
+
+    def __init__(self):
+        self.truncations = 0
+        self.updates = 0
+
+    def reset(self):
+        self.truncations = 0
+        self.updates = 0
+
+    def snapshot(self):
+        return self.truncations, self.updates
+
+    def add(self, truncations, updates):
+        self.truncations += int(truncations)
+        self.updates += int(updates)
+
+
+counters = OpCounters()
+
+_TABLES = {}
+
+
+def table_of(block: Block) -> BlockTable:
+    """Cached BlockTable of the block tree rooted at ``block`` (its root)."""
+    root = block
+    while root.parent is not None:
+        root = root.parent
+    t = _TABLES.get(id(root))
+    if t is None or t.root is not root:
+        t = BlockTable(root)
+        _TABLES[id(root)] = t
+    return t
+
+
+class HMatrix:
+    """View of block ``uid`` of a device-resident H-matrix."""
+
+    __slots__ = ("store", "uid", "policy")
+
+    def __init__(self, store, uid=0, policy=EXACT):
+        self.store = store
+        self.uid = int(uid)
+        self.policy = policy
+
+    # structure ---------------------------------------------------------
+    @property
+    def table(self) -> BlockTable:
+        return self.store.table
+
+    @property
+    def block(self) -> Block:
+        return self.table.blocks[self.uid]
+
+    @property
+    def kind(self):
+        t = self.table
+        if not t.leaf[self.uid]:
+            return BLOCKED
+        return LOWRANK if t.adm[self.uid] else DENSE
+
+    @property
+    def nrows(self):
+        return int(self.table.m[self.uid])
+
+    @property
+    def ncols(self):
+        return int(self.table.nc[self.uid])
+
+    @property
+    def children(self):
+        if self.kind != BLOCKED:
+            return None
+        k = self.table.kids[self.uid]
+        return [[HMatrix(self.store, k[0], self.policy), HMatrix(self.store, k[1], self.policy)],
+                [HMatrix(self.store, k[2], self.policy), HMatrix(self.store, k[3], self.policy)]]
+
+    def child_offsets(self, child):
+        t = self.table
+        return int(t.r0[child.uid] - t.r0[self.uid]), int(t.c0[child.uid] - t.c0[self.uid])
+
+    def leaves(self):
+        for u in self.table.leaves(self.uid):
+            yield HMatrix(self.store, u, self.policy)
+
+    # leaf data (host copies) -------------------------------------------
+    def _leaf(self):
+        return self.store.download_leaf(self.uid)
+
+    @property
+    def D(self):
+        return self._leaf()[1] if self.kind == DENSE else None
+
+    @D.setter
+    def D(self, value):
+        if self.kind != DENSE:
+            raise ValueError("D is defined for dense leaves only")
+        self.store.upload_leaf(self.uid, ("D", np.asarray(value, dtype=float)))
+
+    @property
+    def U(self):
+        return self._leaf()[1] if self.kind == LOWRANK else None
+
+    @property
+    def V(self):
+        return self._leaf()[2] if self.kind == LOWRANK else None
+
+    @property
+    def rank(self) -> int:
+        if self.kind != LOWRANK:
+            raise ValueError("rank defined for low-rank leaves only")
+        return int(self.store.ranks[self.uid].item())
+
+    def set_lowrank(self, U, V):
+        if U.shape[0] != self.nrows or V.shape[0] != self.ncols or U.shape[1] != V.shape[1]:
+            raise ValueError("factor shape mismatch")
+        self.store.upload_leaf(self.uid, ("R", np.asarray(U, float), np.asarray(V, float)))
+
+    # whole-matrix helpers ---------------------------------------------
+    def to_leaves(self):
+        allv = self.store.download_leaves()
+        return {u: allv[u] for u in self.table.leaves(self.uid)}
+
+    def to_dense(self) -> np.ndarray:
+        t = self.table
+        out = np.zeros((self.nrows, self.ncols))
+        for u, x in self.to_leaves().items():
+            blk = x[1] if x[0] == "D" else x[1] @ x[2].T
+            out[t.r0[u] - t.r0[self.uid]:t.r1[u] - t.r0[self.uid],
+                t.c0[u] - t.c0[self.uid]:t.c1[u] - t.c0[self.uid]] = blk
+        return out
+
+    def frobenius(self) -> float:
+        s = 0.0
+        for x in self.to_leaves().values():
+            if x[0] == "D":
+                s += float(np.sum(x[1] * x[1]))
+            else:
+                s += max(0.0, float(((x[1].T @ x[1]) * (x[2].T @ x[2])).sum()))
+        return float(np.sqrt(s))
+
+    def copy(self) -> "HMatrix":
+        if self.uid != 0:
+            raise ValueError("copy() is supported on the root view")
+        return HMatrix(self.store.clone(), 0, self.policy)
+
+    def __repr__(self):
+        return f"HMatrix({self.block!r}, {self.kind})"
+
+
+def _store_cls():
+    from .engine import HStore
+
+    return HStore
+
+
+def _layout(table, rank_cap):
+    from .planner import Layout
+
+    return Layout(table, rank_cap)
+
+
+def zeros(block: Block, policy: TruncationPolicy = EXACT, rank_cap=DEFAULT_RANK_CAP) -> HMatrix:
+    """Zero H-matrix over a block tree (rank-0 admissible leaves, hmatrix.py:251-263)."""
+    t = table_of(block)
+    return HMatrix(_store_cls()(_layout(t, rank_cap)), block.uid, policy)
+
+
+def from_leaves(block: Block, leaves, policy=EXACT, rank_cap=DEFAULT_RANK_CAP) -> HMatrix:
+    """Upload host leaves (uid -> ("D", M) | ("R", U, V)) into device storage."""
+    H = zeros(block, policy, rank_cap)
+    H.store.upload_leaves(leaves)
+    return H
+
+
+def assemble(block: Block, kernel, policy: TruncationPolicy, rank_cap=DEFAULT_RANK_CAP) -> HMatrix:
+    """Evaluate ``kernel`` over the block tree on the device (hmatrix.py:227-248)."""
+    from .assembly import assemble_store
+
+    t = table_of(block)
+    store = _store_cls()(_layout(t, rank_cap))
+    assemble_store(store, kernel, policy)
+    return HMatrix(store, block.uid, policy)
+
+
+def rel_error(A, B) -> float:
+    A = A.to_dense() if isinstance(A, HMatrix) else np.asarray(A, dtype=float)
+    B = B.to_dense() if isinstance(B, HMatrix) else np.asarray(B, dtype=float)
+    num = np.linalg.norm(A - B)
+    den = np.linalg.norm(A)
+    if den == 0.0:
+        return 0.0 if num == 0.0 else float("inf")
+    return float(num / den)
+
+
+def frobenius(M) -> float:
+    return M.frobenius() if isinstance(M, HMatrix) else float(np.linalg.norm(M))
+
+
+def dense_to_lowrank(M, policy):
+    """Device dense_to_lowrank of one block (hmatrix.py:133-138)."""
+    from . import kernels
+
+    counters.add(1, 0)
+    return kernels.dense_to_lowrank(M, policy)
+
+
+def truncate(U, V, policy):
+    """Device truncate of one factor pair (hmatrix.py:113-130)."""
+    from . import kernels
+
+    if U.shape[1] != V.shape[1]:
+        raise ValueError("non-conformal low-rank factors")
+    if U.shape[1] == 0:
+        return U, V
+    counters.add(1, 0)
+    return kernels.truncate(U, V, policy)
+
+
+__all__ = ["TruncationPolicy", "EXACT", "HMatrix", "assemble", "zeros", "from_leaves",
+           "rel_error", "frobenius", "truncate", "dense_to_lowrank", "counters", "DENSE",
+           "LOWRANK", "BLOCKED", "_lib"]

@@ -1,0 +1,115 @@
+"""Device H-LU vs the CPU oracle and the reference fixtures.
+
+Parity bar (BASELINE.json north_star): per-block ranks bit-exact, the
+truncation counter exact, factors within a tolerance tied to eps:
+||L U x - L_ref U_ref x|| / ||L_ref U_ref x|| <= 10 * eps on probe vectors,
+and the probe residual ||A x - L U x|| / ||A x|| within 2x of the
+reference's own residual (or <= 100*eps).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import hm_oracle as O
+from tests.golden_inputs import case, have, load
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_A(name):
+    pts, ell, n_min, kind, eta, eps = case(name)
+    ct = O.cluster_tree(pts, n_min)
+    adm = O.adm_weak(ct) if kind == "weak" else O.adm_standard(ct, eta)
+    bt = O.block_tree(ct, adm)
+    pol = O.Policy("accuracy", eps=eps)
+    A = O.assemble(bt, lambda I, J: O.exp_kernel_dense(pts, ct.perm, ell, I, J), pol)
+    return A, pol, eps
+
+
+def product_structure(name):
+    from paper_1911_07531_b200 import configs
+
+    cfg = configs.config(name)
+    geom, root, perm, broot = configs.structure(cfg)
+    return cfg, broot, perm
+
+
+def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64):
+    from paper_1911_07531_b200 import hmatrix as H
+    from paper_1911_07531_b200.accumulator import AccumulatorMap, hlu_accu
+    from paper_1911_07531_b200.arith import hlu
+
+    cfg, broot, perm = product_structure(name)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.from_leaves(broot, A_leaves, pol, rank_cap)
+    L, U = H.zeros(broot, pol, rank_cap), H.zeros(broot, pol, rank_cap)
+    H.counters.reset()
+    if mode == "std":
+        plan = hlu(A, L, U, pol, exec_mode=exec_mode)
+    else:
+        plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode)
+    return L.store.download_leaves(), U.store.download_leaves(), H.counters.snapshot(), plan
+
+
+@pytest.mark.parametrize("name", ["s1", "s2"])
+@pytest.mark.parametrize("mode", ["std", "accu"])
+def test_hlu_matches_oracle(name, mode):
+    A, pol, eps = oracle_A(name)
+    Lr, Ur, tr, up = O.factor(A, mode, pol)
+    Ld, Ud, (dtr, dup), plan = run_device(name, mode, A.lv)
+    bt = A.bt
+    Lh, Uh = O.HM(bt, Ld), O.HM(bt, Ud)
+    rL, _ = O.leaf_arrays(Lh)
+    rU, _ = O.leaf_arrays(Uh)
+    rLr, _ = O.leaf_arrays(Lr)
+    rUr, _ = O.leaf_arrays(Ur)
+    assert np.array_equal(rL, rLr), np.nonzero(rL != rLr)
+    assert np.array_equal(rU, rUr), np.nonzero(rU != rUr)
+    assert dtr == tr
+    assert dup == up
+    X = np.random.default_rng(5).normal(size=(bt.shape(0)[0], 3))
+    want = O.apply(Lr, 0, O.apply(Ur, 0, X))
+    got = O.apply(Lh, 0, O.apply(Uh, 0, X))
+    assert np.linalg.norm(got - want) <= 10 * eps * np.linalg.norm(want)
+    AX = O.apply(A, 0, X)
+    res = np.linalg.norm(AX - got) / np.linalg.norm(AX)
+    assert res <= 100 * eps
+
+
+@pytest.mark.parametrize("mode", ["std", "accu"])
+def test_executors_bitwise_identical(mode):
+    """wave / graph / persistent / sequential executions give identical bits."""
+    A, pol, eps = oracle_A("s2")
+    outs = []
+    for em in (3, 0, 1, 2):
+        Ld, Ud, _, _ = run_device("s2", mode, A.lv, exec_mode=em)
+        outs.append((Ld, Ud))
+    for Ld, Ud in outs[1:]:
+        for u, x in outs[0][0].items():
+            for a, b in zip(x[1:], Ld[u][1:]):
+                assert np.array_equal(a, b)
+        for u, x in outs[0][1].items():
+            for a, b in zip(x[1:], Ud[u][1:]):
+                assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["c1"])
+def test_reference_fixture_ranks(name):
+    """Ranks/counters equal to the reference's own run (fixture)."""
+    if not have(name):
+        pytest.skip("fixture missing")
+    meta, arr = load(name)
+    A, pol, eps = oracle_A(name)
+    for mode in ("std", "accu"):
+        Ld, Ud, (dtr, dup), _ = run_device(name, mode, A.lv)
+        bt = A.bt
+        rL, _ = O.leaf_arrays(O.HM(bt, Ld))
+        rU, _ = O.leaf_arrays(O.HM(bt, Ud))
+        assert np.array_equal(rL, arr[f"{mode}_L_rank"])
+        assert np.array_equal(rU, arr[f"{mode}_U_rank"])
+        assert dtr == meta[f"{mode}_truncations"]
+        assert dup == meta[f"{mode}_updates"]
+        X = arr["probe_x"]
+        got = O.apply(O.HM(bt, Ld), 0, O.apply(O.HM(bt, Ud), 0, X))
+        want = arr[f"{mode}_probe_LUx"]
+        assert np.linalg.norm(got - want) <= 10 * eps * np.linalg.norm(want)
