@@ -159,6 +159,10 @@ hmx_status hmx_exp_kernel_blocks(int32_t nblocks, const int64_t* desc /* device,
                                  const int64_t* perm, double ell, double diag, double scale,
                                  double* out, void* stream);
 
+/* FP64 FMA-pipe throughput probe (2*8*iters*256*blocks flops), used by
+ * bench.py to measure the FP64 roofline denominator on the box. */
+hmx_status hmx_fp64_fma_probe(int32_t blocks, int32_t iters, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

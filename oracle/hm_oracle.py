@@ -209,9 +209,13 @@ class Policy:
 
 
 class Counters:
+    """Reference counters (hmatrix.py:84-110) plus algorithmic flops of the
+    op trace with SURVEY.md §8d formulas (the device counts the same way)."""
+
     def __init__(self):
         self.truncations = 0
         self.updates = 0
+        self.flops = 0.0
 
 
 COUNT = Counters()
@@ -227,11 +231,30 @@ def truncate(U, V, pol):
     Qv, Rv = np.linalg.qr(V)
     W, s, Zt = np.linalg.svd(Ru @ Rv.T)
     r = pol.keep(s)
+    m, K = U.shape
+    n = V.shape[0]
+    p, q = Ru.shape[0], Rv.shape[0]
+    COUNT.flops += (_qr_f(m, K) + _qr_f(n, K) + 2.0 * p * q * K + _svd_f(p, q)
+                    + 2.0 * m * p * r + 2.0 * n * q * r)
     return Qu @ (W[:, :r] * s[:r]), Qv @ Zt[:r].T
+
+
+def _qr_f(m, k):
+    return 2.0 * (2.0 * m * k * k - 2.0 * k ** 3 / 3.0)
+
+
+def _svd_f(m, n):
+    l, s = max(m, n), min(m, n)
+    return 4.0 * l * s * s + 22.0 * s ** 3
+
+
+def _gemm_f(m, n, k):
+    return 2.0 * m * n * k
 
 
 def dense_to_lowrank(M, pol):
     COUNT.truncations += 1
+    COUNT.flops += _svd_f(*M.shape)
     W, s, Zt = np.linalg.svd(M, full_matrices=False)
     r = pol.keep(s)
     return W[:, :r] * s[:r], Zt[:r].T
@@ -244,6 +267,7 @@ def dense_lu(A):
     U = A.copy()
     L = np.eye(n)
     scale = np.linalg.norm(A)
+    COUNT.flops += 2.0 / 3.0 * n ** 3
     for k in range(n):
         piv = U[k, k]
         if abs(piv) <= PIVOT_CUTOFF * scale:
@@ -310,7 +334,12 @@ def apply(H, u, X):
     bt = H.bt
     if bt.leaf(u):
         x = H.lv[u]
-        return x[1] @ X if x[0] == "D" else x[1] @ (x[2].T @ X)
+        m, n = bt.shape(u)
+        if x[0] == "D":
+            COUNT.flops += _gemm_f(m, X.shape[1], n)
+            return x[1] @ X
+        COUNT.flops += 2.0 * x[1].shape[1] * X.shape[1] * (m + n)
+        return x[1] @ (x[2].T @ X)
     out = np.zeros((bt.shape(u)[0], X.shape[1]))
     for ch in bt.kids[u]:
         r0, c0 = _off(bt, u, ch)
@@ -324,7 +353,12 @@ def apply_t(H, u, X):
     bt = H.bt
     if bt.leaf(u):
         x = H.lv[u]
-        return x[1].T @ X if x[0] == "D" else x[2] @ (x[1].T @ X)
+        m, n = bt.shape(u)
+        if x[0] == "D":
+            COUNT.flops += _gemm_f(n, X.shape[1], m)
+            return x[1].T @ X
+        COUNT.flops += 2.0 * x[1].shape[1] * X.shape[1] * (m + n)
+        return x[2] @ (x[1].T @ X)
     out = np.zeros((bt.shape(u)[1], X.shape[1]))
     for ch in bt.kids[u]:
         r0, c0 = _off(bt, u, ch)
@@ -340,6 +374,7 @@ def solve_lower(L, u, Y):
         x = L.lv[u]
         if x[0] != "D":
             raise ValueError("triangular solve on a low-rank diagonal block")
+        COUNT.flops += float(x[1].shape[0]) ** 2 * Y.shape[1]
         return sla.solve_triangular(x[1], Y, lower=True, unit_diagonal=True)
     k00, _, k10, k11 = bt.kids[u]
     n0 = bt.shape(k00)[0]
@@ -355,6 +390,7 @@ def solve_upper_t(U, u, Y):
         x = U.lv[u]
         if x[0] != "D":
             raise ValueError("triangular solve on a low-rank diagonal block")
+        COUNT.flops += float(x[1].shape[0]) ** 2 * Y.shape[1]
         return sla.solve_triangular(x[1], Y, trans="T", lower=False)
     k00, k01, _, k11 = bt.kids[u]
     n0 = bt.shape(k00)[0]
@@ -392,6 +428,7 @@ def product(alpha, A, ua, B, ub, pol):
     if lb and xb[0] == "R":
         return ("R", apply(A, ua, alpha * xb[1]), xb[2])
     if la and lb:
+        COUNT.flops += _gemm_f(xa[1].shape[0], xb[1].shape[1], xa[1].shape[1])
         return ("D", alpha * (xa[1] @ xb[1]))
     if la:
         return ("D", apply_t(B, ub, alpha * xa[1].T).T)
@@ -420,6 +457,8 @@ def product(alpha, A, ua, B, ub, pol):
                     vs.append(ve)
     if dacc is not None:
         if us:
+            Ku = sum(x.shape[1] for x in us)
+            COUNT.flops += _gemm_f(m, n, Ku)
             dacc += np.hstack(us) @ np.hstack(vs).T
         return ("D", dacc)
     if not us:
@@ -434,9 +473,12 @@ def fold_leaf(C, uc, p, pol):
     COUNT.updates += 1
     x = C.lv[uc]
     if x[0] == "D":
+        if p[0] == "R":
+            COUNT.flops += _gemm_f(p[1].shape[0], p[2].shape[0], p[1].shape[1])
         x[1][...] += p_dense(p)
         return
     if p[0] == "D":
+        COUNT.flops += _gemm_f(x[1].shape[0], x[2].shape[0], x[1].shape[1])
         C.lv[uc] = ("R", *dense_to_lowrank(x[1] @ x[2].T + p[1], pol))
     else:
         C.lv[uc] = ("R", *truncate(np.hstack([x[1], p[1]]), np.hstack([x[2], p[2]]), pol))
@@ -554,6 +596,9 @@ def acc_fold(acc, p, pol):
         acc[0] = ("D", p[1].copy()) if p[0] == "D" else ("R", p[1], p[2])
         return
     if acc[0][0] == "D" or p[0] == "D":
+        for y in (acc[0], p):
+            if y[0] == "R":
+                COUNT.flops += _gemm_f(y[1].shape[0], y[2].shape[0], y[1].shape[1])
         acc[0] = ("D", p_dense(acc[0]) + p_dense(p))
         return
     acc[0] = ("R", *truncate(np.hstack([acc[0][1], p[1]]), np.hstack([acc[0][2], p[2]]), pol))
@@ -681,6 +726,7 @@ def factor(A, mode, pol):
     W = A.copy()
     L, U = zeros(A.bt), zeros(A.bt)
     COUNT.truncations = COUNT.updates = 0
+    COUNT.flops = 0.0
     if mode == "std":
         hlu(W, L, U, 0, pol)
     else:

@@ -94,6 +94,7 @@ def lib():
         "hmx_plan_reset_counters": ([vp, vp], i32),
         "hmx_plan_destroy": ([vp], i32),
         "hmx_exp_kernel_blocks": ([i32, vp, vp, i32, vp, f64, f64, f64, vp, vp], i32),
+        "hmx_fp64_fma_probe": ([i32, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -110,7 +111,7 @@ EXPORTED = (
     "hmx_trsm_upper_trans_batched", "hmx_gemm_batched", "hmx_truncate_batched",
     "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
-    "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_exp_kernel_blocks",
+    "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",
 )
 
 

@@ -401,7 +401,7 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
   if (threadIdx.x == 0) atomicAdd(&P.counters[3], 1ull);
 }
 
-__global__ void __launch_bounds__(HMX_THREADS) k_tasks(DevPlan P, const int* tasks, int ntasks) {
+__global__ void __launch_bounds__(HMX_THREADS, 2) k_tasks(DevPlan P, const int* tasks, int ntasks) {
   extern __shared__ double sm[];
   for (int i = blockIdx.x; i < ntasks; i += gridDim.x) {
     run_task(P, tasks ? tasks[i] : i, sm);
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(HMX_THREADS) k_tasks(DevPlan P, const int* tas
 
 __device__ __forceinline__ int ld_relaxed(int* p) { return atomicAdd(p, 0); }
 
-__global__ void __launch_bounds__(HMX_THREADS) k_persistent(DevPlan P) {
+__global__ void __launch_bounds__(HMX_THREADS, 2) k_persistent(DevPlan P) {
   extern __shared__ double sm[];
   __shared__ int s_task;
   for (;;) {
@@ -473,6 +473,22 @@ __global__ void k_exp_kernel(int nblocks, const int64_t* desc, const double* pts
     }
     o[i + j * m] = v;
   }
+}
+
+// FP64 FMA-pipe peak probe: 8 independent DFMA chains per thread.
+__global__ void k_dfma_peak(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 1e-3 * (threadIdx.x + i);
+  const double b = 0.999999999, c = 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
 int g_num_sms = 0;
@@ -736,6 +752,11 @@ hmx_status hmx_plan_destroy(hmx_plan_t p) {
     if (q) cudaFree(q);
   delete p;
   return HMX_OK;
+}
+
+hmx_status hmx_fp64_fma_probe(int32_t blocks, int32_t iters, double* out, void* stream) {
+  k_dfma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, iters);
+  return cuda_status(cudaGetLastError());
 }
 
 hmx_status hmx_exp_kernel_blocks(int32_t nblocks, const int64_t* desc, const double* points,
