@@ -93,6 +93,7 @@ def lib():
         "hmx_plan_counters": ([vp, vp, C.POINTER(C.c_uint64)], i32),
         "hmx_plan_reset_counters": ([vp, vp], i32),
         "hmx_plan_destroy": ([vp], i32),
+        "hmx_plan_trace": ([vp, i32, vp], i32),
         "hmx_exp_kernel_blocks": ([i32, vp, vp, i32, vp, f64, f64, f64, vp, vp], i32),
         "hmx_fp64_fma_probe": ([i32, i32, vp, vp], i32),
     }
@@ -111,7 +112,7 @@ EXPORTED = (
     "hmx_trsm_upper_trans_batched", "hmx_gemm_batched", "hmx_truncate_batched",
     "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
-    "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",
+    "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_plan_trace", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",
 )
 
 
@@ -171,6 +172,15 @@ class Plan:
 
     def reset_counters(self, stream=None):
         check(lib().hmx_plan_reset_counters(self.h, stream_ptr(stream)), "plan_reset")
+
+    def enable_trace(self, on=True):
+        check(lib().hmx_plan_trace(self.h, int(bool(on)), None), "plan_trace")
+
+    def trace(self):
+        out = np.zeros(3 * self.n_tasks, dtype=np.uint64)
+        check(lib().hmx_plan_trace(self.h, 1, out.ctypes.data_as(C.c_void_p)), "plan_trace")
+        t = out.reshape(-1, 3)
+        return t[:, 0].astype(np.int64), t[:, 1].astype(np.int64), (t[:, 2] & 0xffffffff).astype(np.int64)
 
     def close(self):
         if getattr(self, "h", None):

@@ -116,8 +116,8 @@ def _compress_small(store, tmp, tmp_off, items, policy):
     ws = 0
     for i, u in enumerate(items):
         m, n = int(t.m[u]), int(t.nc[u])
-        s, l = min(m, n), max(m, n)
-        ws = max(ws, 2 * s + s * s + s * l)
+        l = max(m, n)
+        ws = max(ws, 8 * l + 2 * l * l)
         o = ops[i]
         o["code"] = OP_D2LR
         o["dim"][:2] = (m, n)

@@ -375,6 +375,155 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
   return converged;
 }
 
+
+// ---------------------------------------------------------------------------
+// Rank-revealing QR: column-pivoted Householder QR (LAPACK dgeqp3 / dlaqp2
+// conventions) of the p x q matrix G, stopped after k steps as soon as the
+// Frobenius norm of the trailing block G[k:, k:] is <= thr * |R_00|.
+// |R_00| (the largest column norm) is a lower bound of sigma_1, so dropping
+// the trailing block moves every singular value by at most thr*sigma_1
+// (Weyl); the callers use thr = 1e-8 * (keep cut), far below the measured
+// rank margins (SURVEY.md finding 4).  Returns k; perm[c] = original column
+// of pivoted column c; tau[j] the reflector scalars; R in rows 0..k-1.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void argmax_block(double v, int i, double* red, int* ired, double& bv,
+                                             int& bi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (ov > v || (ov == v && oi >= 0 && (i < 0 || oi < i))) { v = ov; i = oi; }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) { red[w] = v; ired[w] = i; }
+  __syncthreads();
+  bv = red[0];
+  bi = ired[0];
+  for (int k = 1; k < HMX_WARPS; ++k)
+    if (red[k] > bv || (red[k] == bv && ired[k] >= 0 && (bi < 0 || ired[k] < bi))) {
+      bv = red[k];
+      bi = ired[k];
+    }
+}
+
+__device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm, double* cn,
+                        double* cn0, double thr, double* red, int* ired) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = w; c < q; c += HMX_WARPS) {
+    const double* g = G + (int64_t)c * ldg;
+    double s = 0.0;
+    for (int i = lane; i < p; i += 32) s = fma(g[i], g[i], s);
+    s = warp_sum(s);
+    if (lane == 0) { cn[c] = s; cn0[c] = s; perm[c] = c; }
+  }
+  __syncthreads();
+  const int kmax = min(p, q);
+  double r00sq = 0.0;
+  int k = 0;
+  for (int j = 0; j < kmax; ++j) {
+    double bv;
+    int bi;
+    {
+      double v = -1.0;
+      int idx = -1;
+      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS)
+        if (cn[c] > v) { v = cn[c]; idx = c; }
+      argmax_block(v, idx, red, ired, bv, bi);
+    }
+    if (j == 0) r00sq = bv;
+    if (!(bv > 0.0)) break;
+    // trailing-norm test (maintained norms first, exact recompute near the cut)
+    double ts = 0.0;
+    for (int c = j + threadIdx.x; c < q; c += HMX_THREADS) ts += cn[c];
+    double tail = block_sum(ts, red);
+    const double lim = thr * thr * r00sq;
+    if (tail <= 4.0 * lim) {
+      __syncthreads();
+      for (int c = j + w; c < q; c += HMX_WARPS) {
+        const double* g = G + (int64_t)c * ldg;
+        double s2 = 0.0;
+        for (int i = j + lane; i < p; i += 32) s2 = fma(g[i], g[i], s2);
+        s2 = warp_sum(s2);
+        if (lane == 0) { cn[c] = s2; cn0[c] = s2; }
+      }
+      __syncthreads();
+      ts = 0.0;
+      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS) ts += cn[c];
+      tail = block_sum(ts, red);
+      if (tail <= lim) break;
+      // re-pick the pivot from the exact norms
+      double v = -1.0;
+      int idx = -1;
+      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS)
+        if (cn[c] > v) { v = cn[c]; idx = c; }
+      argmax_block(v, idx, red, ired, bv, bi);
+    }
+    // swap columns j <-> bi
+    if (bi != j) {
+      double* a = G + (int64_t)j * ldg;
+      double* b = G + (int64_t)bi * ldg;
+      for (int i = threadIdx.x; i < p; i += HMX_THREADS) {
+        const double t = a[i];
+        a[i] = b[i];
+        b[i] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = cn[j]; cn[j] = cn[bi]; cn[bi] = t;
+        t = cn0[j]; cn0[j] = cn0[bi]; cn0[bi] = t;
+        const int pi = perm[j]; perm[j] = perm[bi]; perm[bi] = pi;
+      }
+    }
+    __syncthreads();
+    // Householder reflector of column j (dlarfg)
+    double* x = G + (int64_t)j * ldg;
+    double ss = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < p; i += HMX_THREADS) ss += x[i] * x[i];
+    const double xn2 = block_sum(ss, red);
+    const double alpha = x[j];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    if (xn2 > 0.0)
+      for (int i = j + 1 + threadIdx.x; i < p; i += HMX_THREADS) x[i] *= scal;
+    if (threadIdx.x == 0) { tau[j] = t; x[j] = beta; }
+    __syncthreads();
+    for (int c = j + 1 + w; c < q; c += HMX_WARPS) {
+      double* y = G + (int64_t)c * ldg;
+      if (t != 0.0) {
+        double d = (lane == 0) ? y[j] : 0.0;
+        for (int i = j + 1 + lane; i < p; i += 32) d += x[i] * y[i];
+        d = warp_sum(d) * t;
+        if (lane == 0) y[j] -= d;
+        for (int i = j + 1 + lane; i < p; i += 32) y[i] -= d * x[i];
+      }
+      // norm downdate (dlaqp2): recompute when cancellation is severe
+      __syncwarp();
+      if (lane == 0) {
+        const double rj = y[j];
+        double nv = cn[c] - rj * rj;
+        cn[c] = nv;
+      }
+      __syncwarp();
+      if (!(cn[c] > 1e-4 * cn0[c])) {
+        double s2 = 0.0;
+        for (int i = j + 1 + lane; i < p; i += 32) s2 = fma(y[i], y[i], s2);
+        s2 = warp_sum(s2);
+        if (lane == 0) { cn[c] = s2; cn0[c] = s2; }
+      }
+    }
+    __syncthreads();
+    k = j + 1;
+  }
+  __syncthreads();
+  return k;
+}
+
 // Number of singular values kept — TruncationPolicy.keep (hmatrix.py:62-71).
 // `sig_sorted(i)` = sigma[order[i]]; size = number of singular values.
 __device__ int keep_count(int policy, int fixed_k, double eps, const double* sigma,

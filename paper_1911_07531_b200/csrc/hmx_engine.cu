@@ -47,7 +47,7 @@ enum OpCode : int32_t {
 enum : int32_t { F_TA = 1, F_TB = 2, F_ACC = 4 };
 
 constexpr int kScratchBase = 15;
-constexpr int kSmemDoubles = 12288;  // 96 KB dynamic shared memory per CTA
+constexpr int kSmemDoubles = 26624;  // 208 KB dynamic shared memory, 1 CTA per SM
 constexpr int kSmemWork = kSmemDoubles - 32;
 
 struct DevPlan {
@@ -68,6 +68,7 @@ struct DevPlan {
   int* queue;
   int* qctl;  // [0] head, [1] tail
   int n_tasks;
+  unsigned long long* trace;  // optional: per task (start ns, end ns, smid)
 };
 
 struct Cx {
@@ -113,13 +114,74 @@ __device__ __forceinline__ double svd_flops(double m, double n) {
 }
 
 // ---------------------------------------------------------------------------
-// truncate (hmatrix.py:113-130)
+// low-rank SVD of a dense p x q block G (destroyed):
+//   rank-revealing QR (stopped once the trailing block is below
+//   1e-8 * cut * sigma_1), then one-sided Jacobi on the k x q factor R1^T
+//   (QR-preconditioned, so few sweeps), sorted singular values, keep.
+// Writes dstU (p x r) = W_r Sigma_r and dstV (q x r) = Z_r, G ~ dstU dstV^T.
+// ws: >= 6q + 2q^2 doubles.  smw/smcap: shared work area for X and J.
+// ---------------------------------------------------------------------------
+__device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, double* G, int ldg,
+                           double* ws, double* smw, int smcap, double* dstU, int ldu,
+                           double* dstV, int ldv, double* sm, double* sig_out = nullptr) {
+  double* red = sm;
+  int* ired = reinterpret_cast<int*>(sm + 16);
+  int* flag = reinterpret_cast<int*>(sm + 24);
+  double* tau = ws;
+  double* cn = ws + q;
+  double* cn0 = ws + 2 * q;
+  int* perm = reinterpret_cast<int*>(ws + 3 * q);
+  double* sig = ws + 4 * q;
+  int* ord = reinterpret_cast<int*>(ws + 5 * q);
+  double* rest = ws + 6 * q;
+  const int policy = o.iarg[0];
+  const double cut = (policy == 2) ? o.farg[1] : 1e-14;
+  const double thr = sig_out ? 0.0 : 1e-8 * cut;
+  const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
+  double *X, *J;
+  if (q * k + k * k <= smcap) { X = smw; J = smw + q * k; }
+  else { X = rest; J = rest + (int64_t)q * k; }
+  for (int e = threadIdx.x; e < q * k; e += HMX_THREADS) {
+    const int c = e % q, i = e / q;
+    X[e] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
+  }
+  __syncthreads();
+  if (k > 0 && !cta_jacobi_svd(q, k, X, q, J, k, sig, ord, flag))
+    if (threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
+  if (sig_out) {
+    const int s = min(p, q);
+    for (int t = threadIdx.x; t < s; t += HMX_THREADS) sig_out[t] = (t < k) ? sig[ord[t]] : 0.0;
+    __syncthreads();
+    return k;
+  }
+  int r = keep_count(policy, o.iarg[1], o.farg[1], sig, ord, k);
+  const int cap = o.iarg[2];
+  if (r > cap) {
+    if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW);
+    r = cap;
+  }
+  for (int e = threadIdx.x; e < p * r; e += HMX_THREADS) {
+    const int i = e % p, t = e / p, col = ord[t];
+    dstU[i + (int64_t)t * ldu] = (i < k) ? J[i + col * k] * sig[col] : 0.0;
+  }
+  for (int e = threadIdx.x; e < q * r; e += HMX_THREADS) {
+    const int c = e % q, t = e / q, col = ord[t];
+    dstV[perm[c] + (int64_t)t * ldv] = X[c + col * q] / sig[col];
+  }
+  __syncthreads();
+  cta_apply_q(p, k, G, ldg, tau, r, dstU, ldu);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// truncate (hmatrix.py:113-130): QR(U), QR(V), SVD(Ru Rv^T), keep, recompose
 // ---------------------------------------------------------------------------
 __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
   const int m = o.dim[0], n = o.dim[1];
   const int K = dimv(P, c, o.dim[2]);
   int* rslot = slotp(P, c, o.slot[0]);
   if (K == 0) {  // rank-0 passthrough, not counted (hmatrix.py:121-122)
+    __syncthreads();
     if (threadIdx.x == 0) *rslot = 0;
     __syncthreads();
     return;
@@ -130,52 +192,42 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* Uo = mref(P, c, o.ref[2]);
   double* Vo = mref(P, c, o.ref[3]);
   const int ldu = o.ld[0], ldv = o.ld[1], lduo = o.ld[2], ldvo = o.ld[3];
-  const int kcap = o.iarg[3];
+  const int64_t kb = o.iarg[3];
   double* ws = mref(P, c, o.wref);
   double* tau_u = ws;
-  double* tau_v = ws + kcap;
-  double* sig = ws + 2 * kcap;
-  int* ord = reinterpret_cast<int*>(ws + 3 * kcap);
-  double* gws = ws + 4 * kcap;  // G (kcap*kcap) then J (kcap*kcap)
+  double* tau_v = ws + kb;
+  double* Ruz = ws + 2 * kb;
+  double* Rvz = Ruz + kb * kb;
+  double* Gg = Rvz + kb * kb;
+  double* ws2 = Gg + kb * kb;
   double* red = sm;
-  int* flag = reinterpret_cast<int*>(sm + 8);
   double* work = sm + 32;
 
   cta_householder_qr(m, K, U, ldu, tau_u, red);
   cta_householder_qr(n, K, V, ldv, tau_v, red);
   const int p = min(m, K), q = min(n, K);
-  const bool tr = q > p;                 // Jacobi over the shorter side
-  const int gr = tr ? q : p, gc = tr ? p : q;  // G' is gr x gc, J is gc x gc
-  double *G, *J;
-  if (gr * gc + gc * gc <= kSmemWork) { G = work; J = work + gr * gc; }
-  else { G = gws; J = gws + (int64_t)kcap * kcap; }
-  // G = Ru Rv^T (p x q), or its transpose
-  for (int e = threadIdx.x; e < p * q; e += HMX_THREADS) {
-    const int i = e % p, j = e / p;
-    double s = 0.0;
-    for (int l = max(i, j); l < K; ++l) s = fma(U[i + (int64_t)l * ldu], V[j + (int64_t)l * ldv], s);
-    if (!tr) G[i + j * gr] = s; else G[j + i * gr] = s;
+  for (int e = threadIdx.x; e < p * K; e += HMX_THREADS) {
+    const int i = e % p, l = e / p;
+    Ruz[e] = (l >= i) ? U[i + (int64_t)l * ldu] : 0.0;
   }
+  for (int e = threadIdx.x; e < q * K; e += HMX_THREADS) {
+    const int i = e % q, l = e / q;
+    Rvz[e] = (l >= i) ? V[i + (int64_t)l * ldv] : 0.0;
+  }
+  const bool gsm = p * q + GEMM_SMEM_DOUBLES <= kSmemWork;
+  double* G = gsm ? work : Gg;
   __syncthreads();
-  if (!cta_jacobi_svd(gr, gc, G, gr, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
-  const int size = gc;  // = min(p, q)
-  int r = keep_count(o.iarg[0], o.iarg[1], o.farg[1], sig, ord, size);
-  const int cap = o.iarg[2];
-  if (r > cap) { if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW); r = cap; }
-  // Y_U -> Uo (m x r), Y_V -> Vo (n x r)
-  for (int e = threadIdx.x; e < m * r; e += HMX_THREADS) {
-    const int i = e % m, t = e / m;
-    const int col = ord[t];
-    double v = 0.0;
-    if (i < p) v = !tr ? G[i + col * gr] : J[i + col * gc] * sig[col];
-    Uo[i + (int64_t)t * lduo] = v;
+  cta_gemm(p, q, K, 1.0, Ruz, p, false, Rvz, q, true, false, G, p, gsm ? work + p * q : work);
+  double* smw = gsm ? work + p * q : work;
+  const int smcap = gsm ? kSmemWork - p * q : kSmemWork;
+  const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm);
+  for (int e = threadIdx.x; e < (m - p) * r; e += HMX_THREADS) {
+    const int i = p + e % (m - p), t = e / (m - p);
+    Uo[i + (int64_t)t * lduo] = 0.0;
   }
-  for (int e = threadIdx.x; e < n * r; e += HMX_THREADS) {
-    const int i = e % n, t = e / n;
-    const int col = ord[t];
-    double v = 0.0;
-    if (i < q) v = !tr ? J[i + col * gc] : G[i + col * gr] / sig[col];
-    Vo[i + (int64_t)t * ldvo] = v;
+  for (int e = threadIdx.x; e < (n - q) * r; e += HMX_THREADS) {
+    const int i = q + e % (n - q), t = e / (n - q);
+    Vo[i + (int64_t)t * ldvo] = 0.0;
   }
   __syncthreads();
   cta_apply_q(m, p, U, ldu, tau_u, r, Uo, lduo);
@@ -198,41 +250,23 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   const int ldm = o.ld[0];
   double* Uo = mref(P, c, o.ref[2]);
   double* Vo = mref(P, c, o.ref[3]);
-  const int lduo = o.ld[2], ldvo = o.ld[3];
   double* ws = mref(P, c, o.wref);
-  const int s = min(m, n);
-  const bool tr = n > m;
-  const int gr = tr ? n : m, gc = tr ? m : n;
-  double* sig = ws;
-  int* ord = reinterpret_cast<int*>(ws + s);
-  double* gws = ws + 2 * s;
-  int* flag = reinterpret_cast<int*>(sm + 8);
   double* work = sm + 32;
-  double *G, *J;
-  int ldg;
-  if (gr * gc + gc * gc <= kSmemWork) { G = work; J = work + gr * gc; ldg = gr; }
-  else if (!tr) { G = M; ldg = ldm; J = gws; }
-  else { G = gws + (int64_t)gc * gc; J = gws; ldg = gr; }
-  if (G != M) {
-    for (int e = threadIdx.x; e < gr * gc; e += HMX_THREADS) {
-      const int i = e % gr, j = e / gr;
-      G[i + j * ldg] = !tr ? M[i + (int64_t)j * ldm] : M[j + (int64_t)i * ldm];
-    }
+  double* G = M;
+  int ldg = ldm;
+  const bool gsm = m * n <= kSmemWork / 2 + kSmemWork / 4;
+  if (gsm) {
+    G = work;
+    ldg = m;
+    for (int e = threadIdx.x; e < m * n; e += HMX_THREADS)
+      G[e] = M[(e % m) + (int64_t)(e / m) * ldm];
     __syncthreads();
   }
-  if (!cta_jacobi_svd(gr, gc, G, ldg, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
-  int r = keep_count(o.iarg[0], o.iarg[1], o.farg[1], sig, ord, s);
-  const int cap = o.iarg[2];
-  if (r > cap) { if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW); r = cap; }
-  for (int e = threadIdx.x; e < m * r; e += HMX_THREADS) {
-    const int i = e % m, t = e / m, col = ord[t];
-    Uo[i + (int64_t)t * lduo] = !tr ? G[i + (int64_t)col * ldg] : J[i + col * gc] * sig[col];
-  }
-  for (int e = threadIdx.x; e < n * r; e += HMX_THREADS) {
-    const int i = e % n, t = e / n, col = ord[t];
-    Vo[i + (int64_t)t * ldvo] = !tr ? J[i + col * gc] : G[i + (int64_t)col * ldg] / sig[col];
-  }
+  double* smw = gsm ? work + m * n : work;
+  const int smcap = gsm ? kSmemWork - m * n : kSmemWork;
+  const int r = svd_lowrank(P, o, m, n, G, ldg, ws, smw, smcap, Uo, o.ld[2], Vo, o.ld[3], sm);
   if (threadIdx.x == 0) *rslot = r;
+  const int s = min(m, n);
   count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s + (double)s * n));
   __syncthreads();
 }
@@ -242,21 +276,11 @@ __device__ void op_svals(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* G = mref(P, c, o.ref[0]);
   double* out = mref(P, c, o.ref[2]);
   double* ws = mref(P, c, o.wref);
-  const bool tr = q > p;
-  const int gr = tr ? q : p, gc = tr ? p : q;
-  double* J = ws;
-  double* W = ws + (int64_t)gc * gc;
-  double* sig = W + (int64_t)gr * gc;
-  int* ord = reinterpret_cast<int*>(sig + gc);
-  int* flag = reinterpret_cast<int*>(sm + 8);
-  for (int e = threadIdx.x; e < gr * gc; e += HMX_THREADS) {
-    const int i = e % gr, j = e / gr;
-    W[i + (int64_t)j * gr] = !tr ? G[i + (int64_t)j * o.ld[0]] : G[j + (int64_t)i * o.ld[0]];
-  }
+  double* W = ws + 6 * q + 2 * (int64_t)q * q;
+  for (int e = threadIdx.x; e < p * q; e += HMX_THREADS)
+    W[e] = G[(e % p) + (int64_t)(e / p) * o.ld[0]];
   __syncthreads();
-  if (!cta_jacobi_svd(gr, gc, W, gr, J, gc, sig, ord, flag)) set_status(P, HMX_ERR_NOT_CONVERGED);
-  for (int t = threadIdx.x; t < gc; t += HMX_THREADS) out[t] = sig[ord[t]];
-  __syncthreads();
+  svd_lowrank(P, o, p, q, W, p, ws, sm + 32, kSmemWork, nullptr, 0, nullptr, 0, sm, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -389,7 +413,21 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
   }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+
 __device__ void run_task(const DevPlan& P, int t, double* sm) {
+  unsigned long long t0 = 0;
+  if (P.trace && threadIdx.x == 0) t0 = gtimer();
   Cx c;
   c.scratch = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
   c.rscratch = P.rscratch + (int64_t)blockIdx.x * P.rscratch_stride;
@@ -398,10 +436,17 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
     const hmx_op o = P.ops[i];
     run_op(P, c, o, sm);
   }
-  if (threadIdx.x == 0) atomicAdd(&P.counters[3], 1ull);
+  if (threadIdx.x == 0) {
+    atomicAdd(&P.counters[3], 1ull);
+    if (P.trace) {
+      P.trace[3 * (int64_t)t] = t0;
+      P.trace[3 * (int64_t)t + 1] = gtimer();
+      P.trace[3 * (int64_t)t + 2] = smid() | ((unsigned long long)blockIdx.x << 32);
+    }
+  }
 }
 
-__global__ void __launch_bounds__(HMX_THREADS, 2) k_tasks(DevPlan P, const int* tasks, int ntasks) {
+__global__ void __launch_bounds__(HMX_THREADS, 1) k_tasks(DevPlan P, const int* tasks, int ntasks) {
   extern __shared__ double sm[];
   for (int i = blockIdx.x; i < ntasks; i += gridDim.x) {
     run_task(P, tasks ? tasks[i] : i, sm);
@@ -411,7 +456,7 @@ __global__ void __launch_bounds__(HMX_THREADS, 2) k_tasks(DevPlan P, const int* 
 
 __device__ __forceinline__ int ld_relaxed(int* p) { return atomicAdd(p, 0); }
 
-__global__ void __launch_bounds__(HMX_THREADS, 2) k_persistent(DevPlan P) {
+__global__ void __launch_bounds__(HMX_THREADS, 1) k_persistent(DevPlan P) {
   extern __shared__ double sm[];
   __shared__ int s_task;
   for (;;) {
@@ -547,6 +592,7 @@ struct hmx_plan {
   double* bases[16] = {};
   int* rbases[16] = {};
   cudaGraphExec_t gexec = nullptr;
+  unsigned long long* d_trace = nullptr;
 };
 
 namespace {
@@ -577,6 +623,7 @@ DevPlan make_dev(hmx_plan* p) {
   P.queue = p->d_queue;
   P.qctl = p->d_qctl;
   P.n_tasks = p->n_tasks;
+  P.trace = p->d_trace;
   return P;
 }
 
@@ -644,7 +691,7 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   std::vector<int> seq(nt);
   for (int i = 0; i < nt; ++i) seq[i] = i;
   if (!e) e = upload(&p->d_seq_tasks, seq.data(), (size_t)nt);
-  p->n_ctas = d->max_ctas > 0 ? d->max_ctas : 2 * num_sms();
+  p->n_ctas = d->max_ctas > 0 ? d->max_ctas : num_sms();
   p->scratch_stride = std::max<int64_t>(d->scratch_doubles, 1);
   p->scratch_stride = (p->scratch_stride + 31) & ~int64_t(31);
   p->rscratch_stride = std::max(d->scratch_ranks, 1);
@@ -742,8 +789,26 @@ hmx_status hmx_plan_reset_counters(hmx_plan_t p, void* stream) {
   return cuda_status(e);
 }
 
+hmx_status hmx_plan_trace(hmx_plan_t p, int32_t enable, uint64_t* out) {
+  if (!p) return HMX_ERR_ARG;
+  cudaError_t e = cudaSuccess;
+  if (enable && !p->d_trace) {
+    e = cudaMalloc(&p->d_trace, 3 * (size_t)std::max(p->n_tasks, 1) * sizeof(unsigned long long));
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+  } else if (!enable && p->d_trace && !out) {
+    e = cudaFree(p->d_trace);
+    p->d_trace = nullptr;
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+  }
+  if (!e && out && p->d_trace)
+    e = cudaMemcpy(out, p->d_trace, 3 * (size_t)p->n_tasks * sizeof(unsigned long long),
+                   cudaMemcpyDeviceToHost);
+  return cuda_status(e);
+}
+
 hmx_status hmx_plan_destroy(hmx_plan_t p) {
   if (!p) return HMX_OK;
+  if (p->d_trace) cudaFree(p->d_trace);
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   void* ptrs[] = {p->d_ops, p->d_task_ops, p->d_succ_ptr, p->d_succ_idx, p->d_indeg_init,
                   p->d_indeg, p->d_queue_init, p->d_queue, p->d_qctl, p->d_wave_tasks,
@@ -924,7 +989,7 @@ hmx_status hmx_truncate_batched(int32_t batch, int32_t m, int32_t n, int32_t K, 
   // per-CTA scratch: U copy (m*K), V copy (n*K), workspace 4K + 2K^2
   const int64_t kk = std::max(K, 1);
   const int64_t offV = (int64_t)m * kk, offW = offV + (int64_t)n * kk;
-  const int64_t scratch = offW + 4 * kk + 2 * kk * kk;
+  const int64_t scratch = offW + 8 * kk + 5 * kk * kk;
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);
@@ -963,7 +1028,7 @@ hmx_status hmx_dense_to_lowrank_batched(int32_t batch, int32_t m, int32_t n, con
   if (batch < 0 || m <= 0 || n <= 0 || cap < 0) return HMX_ERR_ARG;
   const int64_t s = std::min(m, n), l = std::max(m, n);
   const int64_t offW = (int64_t)m * n;
-  const int64_t scratch = offW + 2 * s + s * s + s * l;
+  const int64_t scratch = offW + 8 * l + 2 * l * l;
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);
@@ -992,7 +1057,7 @@ hmx_status hmx_svd_values_batched(int32_t batch, int32_t p, int32_t q, const dou
                                   int64_t strideG, double* sigma, int64_t strideS, void* stream) {
   if (batch < 0 || p <= 0 || q <= 0) return HMX_ERR_ARG;
   const int64_t s = std::min(p, q), l = std::max(p, q);
-  const int64_t scratch = s * s + l * s + 2 * s + 2;
+  const int64_t scratch = 8 * (int64_t)q + 2 * (int64_t)q * q + (int64_t)p * q;
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op o = blank(OP_SVALS);
