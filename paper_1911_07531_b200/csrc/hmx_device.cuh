@@ -13,6 +13,11 @@
 #define HMX_THREADS 256
 #endif
 #define HMX_WARPS (HMX_THREADS / 32)
+// 2-D loop over an m x n column-major block without integer division:
+// one warp per column, lanes over rows (coalesced).
+#define FOR_MN(i, j, m, n)                                                  \
+  for (int j = (int)(threadIdx.x >> 5); j < (n); j += HMX_WARPS)            \
+    for (int i = (int)(threadIdx.x & 31); i < (m); i += 32)
 
 namespace hmx {
 
@@ -43,36 +48,21 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // elementwise helpers
 // ---------------------------------------------------------------------------
 __device__ void cta_zero(int m, int n, double* C, int ldc) {
-  const int tot = m * n;
-  for (int e = threadIdx.x; e < tot; e += HMX_THREADS) {
-    const int i = e % m, j = e / m;
-    C[i + (int64_t)j * ldc] = 0.0;
-  }
+  FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] = 0.0;
 }
 
 // C (m x n) = alpha * op(A); transA: A is n x m.
 __device__ void cta_copy(int m, int n, double alpha, const double* A, int lda, bool ta, double* C,
                          int ldc) {
-  const int tot = m * n;
   if (!ta) {
-    for (int e = threadIdx.x; e < tot; e += HMX_THREADS) {
-      const int i = e % m, j = e / m;
-      C[i + (int64_t)j * ldc] = alpha * A[i + (int64_t)j * lda];
-    }
+    FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] = alpha * A[i + (int64_t)j * lda];
   } else {
-    for (int e = threadIdx.x; e < tot; e += HMX_THREADS) {
-      const int j = e % n, i = e / n;  // read A contiguously
-      C[i + (int64_t)j * ldc] = alpha * A[j + (int64_t)i * lda];
-    }
+    FOR_MN(j, i, n, m) C[i + (int64_t)j * ldc] = alpha * A[j + (int64_t)i * lda];
   }
 }
 
 __device__ void cta_add(int m, int n, double alpha, const double* A, int lda, double* C, int ldc) {
-  const int tot = m * n;
-  for (int e = threadIdx.x; e < tot; e += HMX_THREADS) {
-    const int i = e % m, j = e / m;
-    C[i + (int64_t)j * ldc] += alpha * A[i + (int64_t)j * lda];
-  }
+  FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] += alpha * A[i + (int64_t)j * lda];
 }
 
 // ---------------------------------------------------------------------------
@@ -158,8 +148,7 @@ __device__ void cta_gemm(int m, int n, int k, double alpha, const double* __rest
 __device__ bool cta_lu(int n, const double* A, int lda, double* L, int ldl, double* U, int ldu,
                        double* W, double* lv, double* red) {
   double ss = 0.0;
-  for (int e = threadIdx.x; e < n * n; e += HMX_THREADS) {
-    const int i = e % n, j = e / n;
+  FOR_MN(i, j, n, n) {
     const double v = A[i + (int64_t)j * lda];
     W[i + j * n] = v;
     ss += v * v;
@@ -181,8 +170,7 @@ __device__ bool cta_lu(int n, const double* A, int lda, double* L, int ldl, doub
     __syncthreads();
   }
   // write out: L unit lower (zeros above), U upper (zeros below)
-  for (int e = threadIdx.x; e < n * n; e += HMX_THREADS) {
-    const int i = e % n, j = e / n;
+  FOR_MN(i, j, n, n) {
     const double w = W[i + j * n];
     L[i + (int64_t)j * ldl] = (i > j) ? w : (i == j ? 1.0 : 0.0);
     U[i + (int64_t)j * ldu] = (i <= j) ? w : 0.0;
@@ -228,130 +216,162 @@ __device__ void cta_trsm_upper_trans(int n, int c, const double* T, int ldt, dou
 // Householder QR (LAPACK dgeqr2 / dlarfg convention), in place on the
 // m x K matrix A: R in the upper triangle, reflectors v (v0 = 1 implicit)
 // below, tau[j].  np.linalg.qr (hmatrix.py:124-125) returns the same R up to
-// row signs.  One warp per trailing column for the reflector application.
+// row signs.  Per step: warp 0 builds the reflector (one barrier), then one
+// warp per trailing column applies it (one barrier).  Rows are owned by
+// lane (i mod 32) throughout, so no intra-warp hazards arise.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void warp_reflector(int m, int j, double* x, double* tau) {
+  // x = column j; builds H_j = I - tau v v^T with v_j = 1, x[j] := beta
+  const int lane = threadIdx.x & 31;
+  double ss = 0.0;
+  for (int i = j + 1 + ((lane - j - 1) & 31); i < m; i += 32) ss = fma(x[i], x[i], ss);
+  ss = warp_sum(ss);
+  const double alpha = x[j];
+  double t = 0.0, beta = alpha;
+  if (ss > 0.0) {
+    beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+    t = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    for (int i = j + 1 + ((lane - j - 1) & 31); i < m; i += 32) x[i] *= scal;
+  }
+  __syncwarp();
+  if (lane == 0) { tau[j] = t; x[j] = beta; }
+}
+
+// y := H_j y for one column y (whole warp), lane-owned rows i = lane mod 32.
+__device__ __forceinline__ void warp_apply_reflector(int m, int j, const double* v, double t,
+                                                     double* y) {
+  const int lane = threadIdx.x & 31;
+  const int i0 = j + ((lane - j) & 31);  // first owned row >= j
+  double d = 0.0;
+  for (int i = i0; i < m; i += 32) d = fma(i == j ? 1.0 : v[i], y[i], d);
+  d = warp_sum(d) * t;
+  for (int i = i0; i < m; i += 32) y[i] -= d * (i == j ? 1.0 : v[i]);
+}
+
 __device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau, double* red) {
   const int p = min(m, K);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int w = threadIdx.x >> 5;
   for (int j = 0; j < p; ++j) {
     double* x = A + (int64_t)j * lda;
-    double ss = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < m; i += HMX_THREADS) ss += x[i] * x[i];
-    const double xn2 = block_sum(ss, red);
-    const double alpha = x[j];
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
+    if (w == 0) warp_reflector(m, j, x, tau);
     __syncthreads();
-    if (xn2 > 0.0)
-      for (int i = j + 1 + threadIdx.x; i < m; i += HMX_THREADS) x[i] *= scal;
-    if (threadIdx.x == 0) { tau[j] = t; x[j] = beta; }
-    __syncthreads();
-    if (t != 0.0) {
-      for (int c = j + 1 + w; c < K; c += HMX_WARPS) {
-        double* y = A + (int64_t)c * lda;
-        double d = (lane == 0) ? y[j] : 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) d += x[i] * y[i];
-        d = warp_sum(d) * t;
-        if (lane == 0) y[j] -= d;
-        for (int i = j + 1 + lane; i < m; i += 32) y[i] -= d * x[i];
-      }
-    }
+    const double t = tau[j];
+    if (t != 0.0)
+      for (int c = j + 1 + w; c < K; c += HMX_WARPS)
+        warp_apply_reflector(m, j, x, t, A + (int64_t)c * lda);
     __syncthreads();
   }
 }
 
 // X (m x r) := Q X where Q = H_0 H_1 ... H_{p-1} from cta_householder_qr.
+// Columns of X are independent: one warp per column, no block barriers.
 __device__ void cta_apply_q(int m, int p, const double* A, int lda, const double* tau, int r,
                             double* X, int ldx) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int j = p - 1; j >= 0; --j) {
-    const double t = tau[j];
-    if (t != 0.0) {
-      const double* v = A + (int64_t)j * lda;
-      for (int c = w; c < r; c += HMX_WARPS) {
-        double* y = X + (int64_t)c * ldx;
-        double d = (lane == 0) ? y[j] : 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) d += v[i] * y[i];
-        d = warp_sum(d) * t;
-        if (lane == 0) y[j] -= d;
-        for (int i = j + 1 + lane; i < m; i += 32) y[i] -= d * v[i];
-      }
+  const int w = threadIdx.x >> 5;
+  for (int c = w; c < r; c += HMX_WARPS) {
+    double* y = X + (int64_t)c * ldx;
+    for (int j = p - 1; j >= 0; --j) {
+      const double t = tau[j];
+      if (t != 0.0) warp_apply_reflector(m, j, A + (int64_t)j * lda, t, y);
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
 // One-sided (Hestenes) Jacobi SVD of the p x q matrix G (columns rotated in
 // place), accumulating the q x q rotation J (initialised to I here).  On
-// exit G*J_in... : G = W*Sigma (column norms sigma), J = Z.  Parallel
-// round-robin ordering: each round pairs all columns disjointly, one warp
-// per pair.  sigma[q] = column norms, order[q] = column indices sorted by
+// exit G = W*Sigma (column norms sigma) and J = Z.  Parallel round-robin
+// ordering: every round pairs all columns disjointly and ALL pairs of a
+// round run at once, one group of g lanes per pair (g = power of two with
+// (q/2)*g <= threads, g <= 32), with segmented shuffles for the three dot
+// products.  sigma[q] = column norms, order[q] = column indices by
 // descending sigma (ties by index).  Returns false if not converged.
-// The high relative accuracy of one-sided Jacobi keeps singular values near
-// the eps*sigma_1 cut within rounding of LAPACK's dgesdd (hmatrix.py:126).
+// One-sided Jacobi has high relative accuracy, so singular values near the
+// eps*sigma_1 cut agree with LAPACK's dgesdd (hmatrix.py:126) to rounding.
 // ---------------------------------------------------------------------------
-__device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int ldj,
-                               double* sigma, int* order, int* flag) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < q * q; e += HMX_THREADS) {
-    const int i = e % q, j = e / q;
-    J[i + (int64_t)j * ldj] = (i == j) ? 1.0 : 0.0;
-  }
+template <int G>
+__device__ __forceinline__ double seg_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ void jacobi_rounds(int p, int q, double* Gm, int ldg, double* J, int ldj, double tol2,
+                              int* flag) {
   const int qq = q + (q & 1);
+  const int npairs = qq / 2;
+  const int grp = threadIdx.x / G, gl = threadIdx.x % G;
+  const int ngrp = HMX_THREADS / G;
+  for (int rnd = 0; rnd < qq - 1; ++rnd) {
+    for (int pr0 = 0; pr0 < npairs; pr0 += ngrp) {
+      const int pr = pr0 + grp;
+      // circle method: x_i = 1 + (i + rnd) mod (qq-1); pairs (0, x_0), (x_pr, x_{qq-1-pr})
+      const int mq = qq - 1;
+      int a, b;
+      if (pr == 0) { a = 0; b = 1 + rnd; }
+      else {
+        a = pr + rnd; if (a >= mq) a -= mq;
+        a += 1;
+        b = mq - pr + rnd; if (b >= mq) b -= mq;
+        b += 1;
+      }
+      const bool valid = pr < npairs && a < q && b < q;
+      if (a > b) { const int t = a; a = b; b = t; }
+      double al = 0.0, be = 0.0, ga = 0.0;
+      double* x = Gm + (int64_t)a * ldg;
+      double* y = Gm + (int64_t)b * ldg;
+      if (valid)
+        for (int i = gl; i < p; i += G) {
+          const double u = x[i], v = y[i];
+          al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
+        }
+      al = seg_sum<G>(al); be = seg_sum<G>(be); ga = seg_sum<G>(ga);
+      if (!valid || al == 0.0 || be == 0.0 || ga * ga <= tol2 * al * be) continue;
+      const double zeta = (be - al) / (2.0 * ga);
+      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+      const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+      for (int i = gl; i < p; i += G) {
+        const double u = x[i], v = y[i];
+        x[i] = c * u - s * v;
+        y[i] = s * u + c * v;
+      }
+      double* ja = J + (int64_t)a * ldj;
+      double* jb = J + (int64_t)b * ldj;
+      for (int i = gl; i < q; i += G) {
+        const double u = ja[i], v = jb[i];
+        ja[i] = c * u - s * v;
+        jb[i] = s * u + c * v;
+      }
+      if (gl == 0) *flag = 1;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int ldj,
+                               double* sigma, int* order, int* flag, int* sweeps_out = nullptr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  FOR_MN(i, j, q, q) J[i + (int64_t)j * ldj] = (i == j) ? 1.0 : 0.0;
   const double tol = DBL_EPSILON * sqrt((double)max(p, 1));
+  const double tol2 = tol * tol;
+  const int npairs = (q + (q & 1)) / 2;
   bool converged = (q <= 1);
   __syncthreads();
-  for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+  int sweep = 0;
+  for (; sweep < 60 && !converged; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
-    for (int rnd = 0; rnd < qq - 1; ++rnd) {
-      for (int pr = w; pr < qq / 2; pr += HMX_WARPS) {
-        // circle method: x_i = 1 + (i + rnd) % (qq-1); pairs (0,x_0), (x_pr, x_{qq-1-pr})
-        int a, b;
-        if (pr == 0) { a = 0; b = 1 + rnd % (qq - 1); }
-        else {
-          a = 1 + (pr + rnd) % (qq - 1);
-          b = 1 + (qq - 1 - pr + rnd) % (qq - 1);
-        }
-        if (a >= q || b >= q) continue;
-        if (a > b) { const int t = a; a = b; b = t; }
-        double* ga = G + (int64_t)a * ldg;
-        double* gb = G + (int64_t)b * ldg;
-        double al = 0.0, be = 0.0, ga_gb = 0.0;
-        for (int i = lane; i < p; i += 32) {
-          const double x = ga[i], y = gb[i];
-          al = fma(x, x, al); be = fma(y, y, be); ga_gb = fma(x, y, ga_gb);
-        }
-        al = warp_sum(al); be = warp_sum(be); ga_gb = warp_sum(ga_gb);
-        if (al == 0.0 || be == 0.0) continue;
-        if (fabs(ga_gb) <= tol * sqrt(al) * sqrt(be)) continue;
-        const double zeta = (be - al) / (2.0 * ga_gb);
-        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        for (int i = lane; i < p; i += 32) {
-          const double x = ga[i], y = gb[i];
-          ga[i] = c * x - s * y;
-          gb[i] = s * x + c * y;
-        }
-        double* ja = J + (int64_t)a * ldj;
-        double* jb = J + (int64_t)b * ldj;
-        for (int i = lane; i < q; i += 32) {
-          const double x = ja[i], y = jb[i];
-          ja[i] = c * x - s * y;
-          jb[i] = s * x + c * y;
-        }
-        if (lane == 0) *flag = 1;
-      }
-      __syncthreads();
-    }
+    if (npairs * 32 <= HMX_THREADS) jacobi_rounds<32>(p, q, G, ldg, J, ldj, tol2, flag);
+    else if (npairs * 16 <= HMX_THREADS) jacobi_rounds<16>(p, q, G, ldg, J, ldj, tol2, flag);
+    else if (npairs * 8 <= HMX_THREADS) jacobi_rounds<8>(p, q, G, ldg, J, ldj, tol2, flag);
+    else jacobi_rounds<4>(p, q, G, ldg, J, ldj, tol2, flag);
     converged = (*flag == 0);
     __syncthreads();
   }
+  if (sweeps_out) *sweeps_out = sweep;
   // column norms
   for (int c = w; c < q; c += HMX_WARPS) {
     const double* g = G + (int64_t)c * ldg;
@@ -375,7 +395,6 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
   return converged;
 }
 
-
 // ---------------------------------------------------------------------------
 // Rank-revealing QR: column-pivoted Householder QR (LAPACK dgeqp3 / dlaqp2
 // conventions) of the p x q matrix G, stopped after k steps as soon as the
@@ -385,28 +404,9 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
 // (Weyl); the callers use thr = 1e-8 * (keep cut), far below the measured
 // rank margins (SURVEY.md finding 4).  Returns k; perm[c] = original column
 // of pivoted column c; tau[j] the reflector scalars; R in rows 0..k-1.
+// Per step: warp 0 pivots, swaps and builds the reflector (one barrier),
+// all warps apply it and downdate column norms (one barrier).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void argmax_block(double v, int i, double* red, int* ired, double& bv,
-                                             int& bi) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-    if (ov > v || (ov == v && oi >= 0 && (i < 0 || oi < i))) { v = ov; i = oi; }
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) { red[w] = v; ired[w] = i; }
-  __syncthreads();
-  bv = red[0];
-  bi = ired[0];
-  for (int k = 1; k < HMX_WARPS; ++k)
-    if (red[k] > bv || (red[k] == bv && ired[k] >= 0 && (bi < 0 || ired[k] < bi))) {
-      bv = red[k];
-      bi = ired[k];
-    }
-}
-
 __device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm, double* cn,
                         double* cn0, double thr, double* red, int* ired) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -420,26 +420,34 @@ __device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm
   __syncthreads();
   const int kmax = min(p, q);
   double r00sq = 0.0;
-  int k = 0;
+  int* ctl = ired;  // ctl[0]: 0 continue, 1 stop, 2 recompute norms
   for (int j = 0; j < kmax; ++j) {
-    double bv;
-    int bi;
-    {
-      double v = -1.0;
+    if (w == 0) {
+      double v = -1.0, tail = 0.0;
       int idx = -1;
-      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS)
-        if (cn[c] > v) { v = cn[c]; idx = c; }
-      argmax_block(v, idx, red, ired, bv, bi);
+      for (int c = j + lane; c < q; c += 32) {
+        const double x = cn[c];
+        tail += x;
+        if (x > v) { v = x; idx = c; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov > v || (ov == v && oi >= 0 && (idx < 0 || oi < idx))) { v = ov; idx = oi; }
+      }
+      tail = warp_sum(tail);
+      if (j == 0) r00sq = v;
+      const double lim = thr * thr * r00sq;
+      int act = 0;
+      if (!(v > 0.0)) act = 1;
+      else if (tail <= 4.0 * lim) act = 2;
+      if (lane == 0) { ctl[0] = act; ctl[1] = idx; red[0] = r00sq; }
     }
-    if (j == 0) r00sq = bv;
-    if (!(bv > 0.0)) break;
-    // trailing-norm test (maintained norms first, exact recompute near the cut)
-    double ts = 0.0;
-    for (int c = j + threadIdx.x; c < q; c += HMX_THREADS) ts += cn[c];
-    double tail = block_sum(ts, red);
-    const double lim = thr * thr * r00sq;
-    if (tail <= 4.0 * lim) {
-      __syncthreads();
+    __syncthreads();
+    r00sq = red[0];
+    int act = ctl[0];
+    if (act == 2) {  // exact trailing norms near the cut
       for (int c = j + w; c < q; c += HMX_WARPS) {
         const double* g = G + (int64_t)c * ldg;
         double s2 = 0.0;
@@ -448,80 +456,203 @@ __device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm
         if (lane == 0) { cn[c] = s2; cn0[c] = s2; }
       }
       __syncthreads();
-      ts = 0.0;
-      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS) ts += cn[c];
-      tail = block_sum(ts, red);
-      if (tail <= lim) break;
-      // re-pick the pivot from the exact norms
-      double v = -1.0;
-      int idx = -1;
-      for (int c = j + threadIdx.x; c < q; c += HMX_THREADS)
-        if (cn[c] > v) { v = cn[c]; idx = c; }
-      argmax_block(v, idx, red, ired, bv, bi);
-    }
-    // swap columns j <-> bi
-    if (bi != j) {
-      double* a = G + (int64_t)j * ldg;
-      double* b = G + (int64_t)bi * ldg;
-      for (int i = threadIdx.x; i < p; i += HMX_THREADS) {
-        const double t = a[i];
-        a[i] = b[i];
-        b[i] = t;
+      if (w == 0) {
+        double v = -1.0, tail = 0.0;
+        int idx = -1;
+        for (int c = j + lane; c < q; c += 32) {
+          const double x = cn[c];
+          tail += x;
+          if (x > v) { v = x; idx = c; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+          if (ov > v || (ov == v && oi >= 0 && (idx < 0 || oi < idx))) { v = ov; idx = oi; }
+        }
+        tail = warp_sum(tail);
+        if (lane == 0) { ctl[0] = (tail <= thr * thr * r00sq || !(v > 0.0)) ? 1 : 0; ctl[1] = idx; }
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = cn[j]; cn[j] = cn[bi]; cn[bi] = t;
-        t = cn0[j]; cn0[j] = cn0[bi]; cn0[bi] = t;
-        const int pi = perm[j]; perm[j] = perm[bi]; perm[bi] = pi;
+      act = ctl[0];
+    }
+    if (act == 1) return j;
+    if (w == 0) {
+      const int bi = ctl[1];
+      if (bi != j) {
+        double* a = G + (int64_t)j * ldg;
+        double* b = G + (int64_t)bi * ldg;
+        for (int i = lane; i < p; i += 32) {
+          const double t = a[i];
+          a[i] = b[i];
+          b[i] = t;
+        }
+        if (lane == 0) {
+          double t = cn[j]; cn[j] = cn[bi]; cn[bi] = t;
+          t = cn0[j]; cn0[j] = cn0[bi]; cn0[bi] = t;
+          const int pi = perm[j]; perm[j] = perm[bi]; perm[bi] = pi;
+        }
+        __syncwarp();
       }
+      warp_reflector(p, j, G + (int64_t)j * ldg, tau);
     }
     __syncthreads();
-    // Householder reflector of column j (dlarfg)
-    double* x = G + (int64_t)j * ldg;
-    double ss = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < p; i += HMX_THREADS) ss += x[i] * x[i];
-    const double xn2 = block_sum(ss, red);
-    const double alpha = x[j];
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    __syncthreads();
-    if (xn2 > 0.0)
-      for (int i = j + 1 + threadIdx.x; i < p; i += HMX_THREADS) x[i] *= scal;
-    if (threadIdx.x == 0) { tau[j] = t; x[j] = beta; }
-    __syncthreads();
+    const double t = tau[j];
+    const double* x = G + (int64_t)j * ldg;
     for (int c = j + 1 + w; c < q; c += HMX_WARPS) {
       double* y = G + (int64_t)c * ldg;
-      if (t != 0.0) {
-        double d = (lane == 0) ? y[j] : 0.0;
-        for (int i = j + 1 + lane; i < p; i += 32) d += x[i] * y[i];
-        d = warp_sum(d) * t;
-        if (lane == 0) y[j] -= d;
-        for (int i = j + 1 + lane; i < p; i += 32) y[i] -= d * x[i];
-      }
-      // norm downdate (dlaqp2): recompute when cancellation is severe
+      if (t != 0.0) warp_apply_reflector(p, j, x, t, y);
       __syncwarp();
-      if (lane == 0) {
-        const double rj = y[j];
-        double nv = cn[c] - rj * rj;
-        cn[c] = nv;
-      }
+      const double rj = y[j];
+      const double nv = cn[c] - rj * rj;
+      const bool rec = !(nv > 1e-4 * cn0[c]);
       __syncwarp();
-      if (!(cn[c] > 1e-4 * cn0[c])) {
+      if (rec) {  // dlaqp2: recompute after severe cancellation
         double s2 = 0.0;
         for (int i = j + 1 + lane; i < p; i += 32) s2 = fma(y[i], y[i], s2);
         s2 = warp_sum(s2);
         if (lane == 0) { cn[c] = s2; cn0[c] = s2; }
+      } else if (lane == 0) {
+        cn[c] = nv;
       }
     }
     __syncthreads();
-    k = j + 1;
+  }
+  return kmax;
+}
+
+// ---------------------------------------------------------------------------
+// Blocked Householder QR (LAPACK dgeqrf) of a tall m x K matrix A in global
+// memory: panels of QR_NB columns are factored in shared memory
+// (cta_householder_qr), the block reflector I - V T V^T is formed (dlarft)
+// and the trailing columns are updated with two GEMMs.  V is also kept
+// explicitly (unit lower, Vx m x p) with the T blocks (Tb, NB x NB each) so
+// that Q can later be applied as GEMMs (cta_apply_q_blocked).
+// ---------------------------------------------------------------------------
+constexpr int QR_NB = 16;
+
+// Panel width of the blocked QR for m rows: as wide as fits (panel + T +
+// GEMM staging) in the shared work area, between 4 and QR_NB.
+__device__ __forceinline__ int qr_nb(int m, int smcap) {
+  int nb = (smcap - QR_NB * QR_NB - GEMM_SMEM_DOUBLES) / max(m, 1);
+  return max(4, min(QR_NB, nb));
+}
+
+// T (jb x jb, ld QR_NB) of the block reflector from explicit V (rows x jb).
+__device__ void cta_larft(int rows, int jb, const double* V, int ldv, const double* tau, double* T,
+                          double* S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int e = w; e < jb * jb; e += HMX_WARPS) {
+    const int i = e % jb, j = e / jb;
+    if (i >= j) continue;
+    const double* vi = V + (int64_t)i * ldv;
+    const double* vj = V + (int64_t)j * ldv;
+    double d = 0.0;
+    for (int r = j + lane; r < rows; r += 32) d = fma(vi[r], vj[r], d);
+    d = warp_sum(d);
+    if (lane == 0) S[i + j * QR_NB] = d;
   }
   __syncthreads();
-  return k;
+  if (w == 0) {
+    for (int j = 0; j < jb; ++j) {
+      // T[0:j, j] = -tau_j * T[0:j, 0:j] * S[0:j, j];  T[j, j] = tau_j
+      double v = 0.0;
+      if (lane < j) {
+        for (int l = lane; l < j; ++l) v = fma(T[lane + l * QR_NB], S[l + j * QR_NB], v);
+        v *= -tau[j];
+      }
+      __syncwarp();
+      if (lane < j) T[lane + j * QR_NB] = v;
+      if (lane == 0) T[j + j * QR_NB] = tau[j];
+      for (int i = j + 1 + lane; i < jb; i += 32) T[i + j * QR_NB] = 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// Y (jb x nc, ld ldy) := op(T) * Y for upper-triangular T (ld QR_NB)
+__device__ void cta_trmm_small(int jb, int nc, const double* T, bool trans, double* Y, int ldy,
+                               double* tmp) {
+  for (int e = threadIdx.x; e < jb * nc; e += HMX_THREADS) {
+    const int i = e % jb, c = e / jb;
+    double v = 0.0;
+    if (!trans) {
+      for (int l = i; l < jb; ++l) v = fma(T[i + l * QR_NB], Y[l + (int64_t)c * ldy], v);
+    } else {
+      for (int l = 0; l <= i; ++l) v = fma(T[l + i * QR_NB], Y[l + (int64_t)c * ldy], v);
+    }
+    tmp[e] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < jb * nc; e += HMX_THREADS) {
+    const int i = e % jb, c = e / jb;
+    Y[i + (int64_t)c * ldy] = tmp[e];
+  }
+  __syncthreads();
+}
+
+// ws (global): W (QR_NB x K) + tmp (QR_NB x K).  sm: shared work area of
+// smcap doubles (panel staging + GEMM staging).
+__device__ void cta_qr_blocked(int m, int K, double* A, int lda, double* tau, double* Vx, int ldv,
+                               double* Tb, double* ws, double* sm, int smcap, double* red) {
+  const int p = min(m, K);
+  const int nb = qr_nb(m, smcap);
+  double* S = sm;                      // QR_NB^2
+  double* panel = sm + QR_NB * QR_NB;  // rows x jb
+  double* gsm = panel;                 // GEMM staging (after the panel is written back)
+  for (int j0 = 0; j0 < p; j0 += nb) {
+    const int jb = min(nb, p - j0);
+    const int rows = m - j0;
+    double* Ap = A + j0 + (int64_t)j0 * lda;
+    const bool psm = rows * jb + QR_NB * QR_NB <= smcap && GEMM_SMEM_DOUBLES + QR_NB * QR_NB <= smcap;
+    double* P = psm ? panel : Ap;
+    const int ldp = psm ? rows : lda;
+    if (psm) {
+      FOR_MN(i, c, rows, jb) P[i + c * rows] = Ap[i + (int64_t)c * lda];
+      __syncthreads();
+    }
+    cta_householder_qr(rows, jb, P, ldp, tau + j0, red);
+    double* Vp = Vx + j0 + (int64_t)j0 * ldv;
+    FOR_MN(i, c, rows, jb) {
+      const double v = P[i + (int64_t)c * ldp];
+      Vp[i + (int64_t)c * ldv] = (i > c) ? v : (i == c ? 1.0 : 0.0);
+      if (psm) Ap[i + (int64_t)c * lda] = v;
+    }
+    __syncthreads();
+    double* T = Tb + (int64_t)(j0 / nb) * QR_NB * QR_NB;
+    cta_larft(rows, jb, Vp, ldv, tau + j0, T, S);
+    const int nc = K - j0 - jb;
+    if (nc > 0) {
+      double* C = A + j0 + (int64_t)(j0 + jb) * lda;
+      double* W = ws;
+      double* tmp = ws + (int64_t)QR_NB * K;
+      cta_gemm(jb, nc, rows, 1.0, Vp, ldv, true, C, lda, false, false, W, QR_NB, gsm);
+      cta_trmm_small(jb, nc, T, true, W, QR_NB, tmp);
+      cta_gemm(rows, nc, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, C, lda, gsm);
+    }
+  }
+}
+
+// X (m x r) := Q X with Q = (I - V0 T0 V0^T)(I - V1 T1 V1^T)...
+// ws: W (QR_NB x r) + tmp (QR_NB x r)
+__device__ void cta_apply_q_blocked(int m, int p, const double* Vx, int ldv, const double* Tb,
+                                    int r, double* X, int ldx, double* ws, double* gsm,
+                                    int smcap) {
+  if (r == 0) return;
+  const int nb = qr_nb(m, smcap);
+  const int nblk = (p + nb - 1) / nb;
+  double* W = ws;
+  double* tmp = ws + (int64_t)QR_NB * r;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * nb, jb = min(nb, p - j0), rows = m - j0;
+    const double* Vp = Vx + j0 + (int64_t)j0 * ldv;
+    const double* T = Tb + (int64_t)b * QR_NB * QR_NB;
+    double* Xp = X + j0;
+    cta_gemm(jb, r, rows, 1.0, Vp, ldv, true, Xp, ldx, false, false, W, QR_NB, gsm);
+    cta_trmm_small(jb, r, T, false, W, QR_NB, tmp);
+    cta_gemm(rows, r, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, Xp, ldx, gsm);
+  }
 }
 
 // Number of singular values kept — TruncationPolicy.keep (hmatrix.py:62-71).

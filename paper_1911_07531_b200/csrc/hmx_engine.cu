@@ -121,6 +121,25 @@ __device__ __forceinline__ double svd_flops(double m, double n) {
 // Writes dstU (p x r) = W_r Sigma_r and dstV (q x r) = Z_r, G ~ dstU dstV^T.
 // ws: >= 6q + 2q^2 doubles.  smw/smcap: shared work area for X and J.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long gtimer2() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+// phase profile (trace mode): slots 12..15 of the per-opcode table:
+// 12 = Householder QR of the stacked factors, 13 = RRQR, 14 = Jacobi
+// (count field = sweeps), 15 = recomposition (Q applications)
+__device__ __forceinline__ void phase(const DevPlan& P, int slot, unsigned long long& t0,
+                                      unsigned long long cnt = 1) {
+  if (P.trace && threadIdx.x == 0) {
+    const unsigned long long t1 = gtimer2();
+    unsigned long long* prof = P.trace + 3 * (int64_t)P.n_tasks;
+    atomicAdd(&prof[2 * slot], t1 - t0);
+    atomicAdd(&prof[2 * slot + 1], cnt);
+    t0 = t1;
+  }
+}
+
 __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, double* G, int ldg,
                            double* ws, double* smw, int smcap, double* dstU, int ldu,
                            double* dstV, int ldv, double* sm, double* sig_out = nullptr) {
@@ -137,17 +156,18 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
   const double thr = sig_out ? 0.0 : 1e-8 * cut;
+  unsigned long long t0 = P.trace ? gtimer2() : 0;
   const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
+  phase(P, 13, t0);
   double *X, *J;
   if (q * k + k * k <= smcap) { X = smw; J = smw + q * k; }
   else { X = rest; J = rest + (int64_t)q * k; }
-  for (int e = threadIdx.x; e < q * k; e += HMX_THREADS) {
-    const int c = e % q, i = e / q;
-    X[e] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
-  }
+  FOR_MN(c, i, q, k) X[c + i * q] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
   __syncthreads();
-  if (k > 0 && !cta_jacobi_svd(q, k, X, q, J, k, sig, ord, flag))
+  int sweeps = 0;
+  if (k > 0 && !cta_jacobi_svd(q, k, X, q, J, k, sig, ord, flag, &sweeps))
     if (threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
+  phase(P, 14, t0, sweeps);
   if (sig_out) {
     const int s = min(p, q);
     for (int t = threadIdx.x; t < s; t += HMX_THREADS) sig_out[t] = (t < k) ? sig[ord[t]] : 0.0;
@@ -160,12 +180,12 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
     if (threadIdx.x == 0) set_status(P, HMX_ERR_RANK_OVERFLOW);
     r = cap;
   }
-  for (int e = threadIdx.x; e < p * r; e += HMX_THREADS) {
-    const int i = e % p, t = e / p, col = ord[t];
+  FOR_MN(i, t, p, r) {
+    const int col = ord[t];
     dstU[i + (int64_t)t * ldu] = (i < k) ? J[i + col * k] * sig[col] : 0.0;
   }
-  for (int e = threadIdx.x; e < q * r; e += HMX_THREADS) {
-    const int c = e % q, t = e / q, col = ord[t];
+  FOR_MN(c, t, q, r) {
+    const int col = ord[t];
     dstV[perm[c] + (int64_t)t * ldv] = X[c + col * q] / sig[col];
   }
   __syncthreads();
@@ -187,6 +207,7 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     return;
   }
   if (threadIdx.x == 0) atomicAdd(&P.counters[0], 1ull);
+  unsigned long long tq = P.trace ? gtimer2() : 0;
   double* U = mref(P, c, o.ref[0]);
   double* V = mref(P, c, o.ref[1]);
   double* Uo = mref(P, c, o.ref[2]);
@@ -199,39 +220,73 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* Ruz = ws + 2 * kb;
   double* Rvz = Ruz + kb * kb;
   double* Gg = Rvz + kb * kb;
-  double* ws2 = Gg + kb * kb;
+  double* ws2 = Gg + kb * kb;                 // svd_lowrank: 6kb + 2kb^2
+  double* Vxu = ws2 + 6 * kb + 2 * kb * kb;   // explicit reflectors of U (m x kb)
+  double* Vxv = Vxu + (int64_t)m * kb;        // ... of V (n x kb)
+  const int64_t tsz = (kb / 4 + 1) * QR_NB * QR_NB;
+  double* Tu = Vxv + (int64_t)n * kb;
+  double* Tv = Tu + tsz;
+  double* Wq = Tv + tsz;                      // 2 * QR_NB * kb
   double* red = sm;
   double* work = sm + 32;
-
-  cta_householder_qr(m, K, U, ldu, tau_u, red);
-  cta_householder_qr(n, K, V, ldv, tau_v, red);
   const int p = min(m, K), q = min(n, K);
-  for (int e = threadIdx.x; e < p * K; e += HMX_THREADS) {
-    const int i = e % p, l = e / p;
-    Ruz[e] = (l >= i) ? U[i + (int64_t)l * ldu] : 0.0;
+  // stage U, V (and G) in shared memory when they fit
+  const int64_t need = (int64_t)(m + n) * K + 2 * K + (int64_t)p * q;
+  const bool stage = need + 2048 <= kSmemWork;
+  double* G;
+  double* smw;
+  int smcap;
+  if (stage) {
+    double* Us = work;
+    double* Vs = Us + m * K;
+    tau_u = Vs + n * K;
+    tau_v = tau_u + K;
+    G = tau_v + K;
+    FOR_MN(i, l, m, K) Us[i + l * m] = U[i + (int64_t)l * ldu];
+    FOR_MN(i, l, n, K) Vs[i + l * n] = V[i + (int64_t)l * ldv];
+    __syncthreads();
+    U = Us;
+    V = Vs;
+    cta_householder_qr(m, K, U, m, tau_u, red);
+    cta_householder_qr(n, K, V, n, tau_v, red);
+    FOR_MN(i, j, p, q) {
+      double acc = 0.0;
+      for (int l = max(i, j); l < K; ++l) acc = fma(U[i + l * m], V[j + l * n], acc);
+      G[i + j * p] = acc;
+    }
+    __syncthreads();
+    smw = G + p * q;
+    smcap = (int)(kSmemWork - need);
+  } else {
+    cta_qr_blocked(m, K, U, ldu, tau_u, Vxu, m, Tu, Wq, work, kSmemWork, red);
+    cta_qr_blocked(n, K, V, ldv, tau_v, Vxv, n, Tv, Wq, work, kSmemWork, red);
+    FOR_MN(i, l, p, K) Ruz[i + l * p] = (l >= i) ? U[i + (int64_t)l * ldu] : 0.0;
+    FOR_MN(i, l, q, K) Rvz[i + l * q] = (l >= i) ? V[i + (int64_t)l * ldv] : 0.0;
+    // shared memory goes to the Jacobi factors first (X q x k, J k x k);
+    // the core G lives there too only when all three fit
+    const int s_ = min(p, q);
+    const bool gsm = p * q + q * s_ + s_ * s_ + GEMM_SMEM_DOUBLES <= kSmemWork;
+    G = gsm ? work : Gg;
+    __syncthreads();
+    cta_gemm(p, q, K, 1.0, Ruz, p, false, Rvz, q, true, false, G, p, gsm ? work + p * q : work);
+    smw = gsm ? work + p * q : work;
+    smcap = gsm ? kSmemWork - p * q : kSmemWork;
   }
-  for (int e = threadIdx.x; e < q * K; e += HMX_THREADS) {
-    const int i = e % q, l = e / q;
-    Rvz[e] = (l >= i) ? V[i + (int64_t)l * ldv] : 0.0;
-  }
-  const bool gsm = p * q + GEMM_SMEM_DOUBLES <= kSmemWork;
-  double* G = gsm ? work : Gg;
-  __syncthreads();
-  cta_gemm(p, q, K, 1.0, Ruz, p, false, Rvz, q, true, false, G, p, gsm ? work + p * q : work);
-  double* smw = gsm ? work + p * q : work;
-  const int smcap = gsm ? kSmemWork - p * q : kSmemWork;
+  const int ldu_q = stage ? m : ldu, ldv_q = stage ? n : ldv;
+  phase(P, 12, tq);
   const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm);
-  for (int e = threadIdx.x; e < (m - p) * r; e += HMX_THREADS) {
-    const int i = p + e % (m - p), t = e / (m - p);
-    Uo[i + (int64_t)t * lduo] = 0.0;
-  }
-  for (int e = threadIdx.x; e < (n - q) * r; e += HMX_THREADS) {
-    const int i = q + e % (n - q), t = e / (n - q);
-    Vo[i + (int64_t)t * ldvo] = 0.0;
-  }
+  if (P.trace && threadIdx.x == 0) tq = gtimer2();
+  FOR_MN(i, t, m - p, r) Uo[p + i + (int64_t)t * lduo] = 0.0;
+  FOR_MN(i, t, n - q, r) Vo[q + i + (int64_t)t * ldvo] = 0.0;
   __syncthreads();
-  cta_apply_q(m, p, U, ldu, tau_u, r, Uo, lduo);
-  cta_apply_q(n, q, V, ldv, tau_v, r, Vo, ldvo);
+  if (stage) {
+    cta_apply_q(m, p, U, ldu_q, tau_u, r, Uo, lduo);
+    cta_apply_q(n, q, V, ldv_q, tau_v, r, Vo, ldvo);
+  } else {
+    cta_apply_q_blocked(m, p, Vxu, m, Tu, r, Uo, lduo, Wq, work, kSmemWork);
+    cta_apply_q_blocked(n, q, Vxv, n, Tv, r, Vo, ldvo, Wq, work, kSmemWork);
+  }
+  phase(P, 15, tq);
   if (threadIdx.x == 0) *rslot = r;
   count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) +
                2.0 * m * p * r + 2.0 * n * q * r,
@@ -258,8 +313,7 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   if (gsm) {
     G = work;
     ldg = m;
-    for (int e = threadIdx.x; e < m * n; e += HMX_THREADS)
-      G[e] = M[(e % m) + (int64_t)(e / m) * ldm];
+    FOR_MN(i, j, m, n) G[i + j * m] = M[i + (int64_t)j * ldm];
     __syncthreads();
   }
   double* smw = gsm ? work + m * n : work;
@@ -344,24 +398,20 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       double* Ts = work;
       const bool stageT = n * n <= kSmemWork;
       if (stageT) {
-        for (int e = threadIdx.x; e < n * n; e += HMX_THREADS)
-          Ts[e] = T[(e % n) + (int64_t)(e / n) * ldt];
+        FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];
         T = Ts;
         ldt = n;
       }
       double* Bs = work + (stageT ? n * n : 0);
       const bool stageB = stageT && (n * n + n * cc <= kSmemWork);
-      if (stageB)
-        for (int e = threadIdx.x; e < n * cc; e += HMX_THREADS)
-          Bs[e] = B[(e % n) + (int64_t)(e / n) * ldb];
+      if (stageB) FOR_MN(i, j, n, cc) Bs[i + j * n] = B[i + (int64_t)j * ldb];
       __syncthreads();
       double* Bw = stageB ? Bs : B;
       const int ldw = stageB ? n : ldb;
       if (o.code == OP_TRSM_LL) cta_trsm_lower_unit(n, cc, T, ldt, Bw, ldw);
       else cta_trsm_upper_trans(n, cc, T, ldt, Bw, ldw);
       if (stageB) {
-        for (int e = threadIdx.x; e < n * cc; e += HMX_THREADS)
-          B[(e % n) + (int64_t)(e / n) * ldb] = Bs[e];
+        FOR_MN(i, j, n, cc) B[i + (int64_t)j * ldb] = Bs[i + j * n];
         __syncthreads();
       }
       count(P, (double)n * n * cc, 8.0 * ((double)n * n / 2.0 + 2.0 * n * cc));
@@ -394,16 +444,12 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       const double* Vs = mref(P, c, o.ref[1]);
       double* Ud = mref(P, c, o.ref[2]) + (int64_t)col0 * o.ld[2];
       double* Vd = mref(P, c, o.ref[3]) + (int64_t)col0 * o.ld[3];
-      for (int e = threadIdx.x; e < M * k; e += HMX_THREADS) {
-        const int i = e % M, t = e / M;
+      FOR_MN(i, t, M, k)
         Ud[i + (int64_t)t * o.ld[2]] =
             (i >= r0 && i < r0 + mq) ? Us[(i - r0) + (int64_t)t * o.ld[0]] : 0.0;
-      }
-      for (int e = threadIdx.x; e < N * k; e += HMX_THREADS) {
-        const int i = e % N, t = e / N;
+      FOR_MN(i, t, N, k)
         Vd[i + (int64_t)t * o.ld[3]] =
             (i >= c0 && i < c0 + nq) ? Vs[(i - c0) + (int64_t)t * o.ld[1]] : 0.0;
-      }
       __syncthreads();
       if (threadIdx.x == 0) *cnt = col0 + k;
       __syncthreads();
@@ -434,7 +480,15 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
   const int64_t b = P.task_ops[t], e = P.task_ops[t + 1];
   for (int64_t i = b; i < e; ++i) {
     const hmx_op o = P.ops[i];
+    unsigned long long q0 = 0;
+    if (P.trace && threadIdx.x == 0) q0 = gtimer();
     run_op(P, c, o, sm);
+    if (P.trace && threadIdx.x == 0) {
+      // per-opcode busy time and count, after the task records (3*n_tasks words)
+      unsigned long long* prof = P.trace + 3 * (int64_t)P.n_tasks;
+      atomicAdd(&prof[2 * (o.code & 15)], gtimer() - q0);
+      atomicAdd(&prof[2 * (o.code & 15) + 1], 1ull);
+    }
   }
   if (threadIdx.x == 0) {
     atomicAdd(&P.counters[3], 1ull);
@@ -786,6 +840,9 @@ hmx_status hmx_plan_reset_counters(hmx_plan_t p, void* stream) {
   cudaError_t e = cudaMemsetAsync(p->d_counters, 0, 4 * sizeof(unsigned long long),
                                   (cudaStream_t)stream);
   if (!e) e = cudaMemsetAsync(p->d_status, 0, sizeof(int), (cudaStream_t)stream);
+  if (!e && p->d_trace)
+    e = cudaMemsetAsync(p->d_trace + 3 * (size_t)p->n_tasks, 0, 32 * sizeof(unsigned long long),
+                        (cudaStream_t)stream);
   return cuda_status(e);
 }
 
@@ -793,7 +850,7 @@ hmx_status hmx_plan_trace(hmx_plan_t p, int32_t enable, uint64_t* out) {
   if (!p) return HMX_ERR_ARG;
   cudaError_t e = cudaSuccess;
   if (enable && !p->d_trace) {
-    e = cudaMalloc(&p->d_trace, 3 * (size_t)std::max(p->n_tasks, 1) * sizeof(unsigned long long));
+    e = cudaMalloc(&p->d_trace, (3 * (size_t)std::max(p->n_tasks, 1) + 32) * sizeof(unsigned long long));
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
   } else if (!enable && p->d_trace && !out) {
     e = cudaFree(p->d_trace);
@@ -801,7 +858,7 @@ hmx_status hmx_plan_trace(hmx_plan_t p, int32_t enable, uint64_t* out) {
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
   }
   if (!e && out && p->d_trace)
-    e = cudaMemcpy(out, p->d_trace, 3 * (size_t)p->n_tasks * sizeof(unsigned long long),
+    e = cudaMemcpy(out, p->d_trace, (3 * (size_t)p->n_tasks + 32) * sizeof(unsigned long long),
                    cudaMemcpyDeviceToHost);
   return cuda_status(e);
 }
@@ -989,7 +1046,7 @@ hmx_status hmx_truncate_batched(int32_t batch, int32_t m, int32_t n, int32_t K, 
   // per-CTA scratch: U copy (m*K), V copy (n*K), workspace 4K + 2K^2
   const int64_t kk = std::max(K, 1);
   const int64_t offV = (int64_t)m * kk, offW = offV + (int64_t)n * kk;
-  const int64_t scratch = offW + 8 * kk + 5 * kk * kk;
+  const int64_t scratch = offW + 5 * kk * kk + (int64_t)(m + n + 200) * kk + 2048;
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);

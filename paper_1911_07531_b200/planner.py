@@ -255,7 +255,7 @@ class Planner:
 
     def trunc(self, m, n, K, kb, U, V, Uo, Vo, rslot, cap):
         kb = max(int(kb), 1)
-        ws = self.sref(8 * kb + 5 * kb * kb, 1)
+        ws = self.sref(5 * kb * kb + (int(m) + int(n) + 200) * kb + 2048, 1)
         self._op(OP_TRUNC, 0, (m, n, K, 0), (U.ld, V.ld, Uo.ld, Vo.ld), (U, V, Uo, Vo),
                  slots=(rslot, 0, 0, 0), iargs=(self.mode, self.kfix, cap, kb),
                  fargs=(0.0, self.eps), wref=ws)

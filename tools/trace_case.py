@@ -33,6 +33,12 @@ st, en, sm = plan.plan.trace()
 dur = (en - st) / 1e3  # us
 span = (en.max() - st.min()) / 1e6
 kinds = np.array(plan.prog.kinds)
+names = {1:"GEMM",2:"COPY",3:"ZERO",4:"ADD",5:"LU",6:"TRSM_LL",7:"TRSM_UT",8:"TRUNC",9:"D2LR",10:"SETRANK",11:"APPEND",
+         12:"tr.QR", 13:"svd.RRQR", 14:"svd.Jacobi(n=sweeps)", 15:"tr.recomp"}
+prof = plan.plan.op_profile
+for code in range(16):
+    if prof[code, 1]:
+        print(f"  op {names.get(code, code):8s} n={prof[code,1]:8d} busy={prof[code,0]/1e6:9.2f} ms mean={prof[code,0]/prof[code,1]/1e3:8.1f} us")
 print(f"{name} {mode} exec={exe}: wall {wall*1e3:.1f} ms, device span {span:.1f} ms, tasks {len(dur)}")
 print("busy sum %.1f ms -> mean parallelism %.1f" % (dur.sum() / 1e3, dur.sum() / 1e3 / span))
 for k in sorted(set(kinds)):
