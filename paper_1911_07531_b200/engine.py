@@ -52,6 +52,21 @@ class HStore:
     def clone(self):
         return HStore(self.layout, self.values.clone(), self.ranks.clone())
 
+    @classmethod
+    def batch(cls, layout: Layout, nrep: int):
+        """nrep same-layout matrices in one contiguous pool (batched plans)."""
+        torch = _torch()
+        values = torch.zeros(layout.size * nrep, dtype=torch.float64, device="cuda")
+        r = np.full(layout.table.n, -1, dtype=np.int32)
+        r[layout.table.leaf & layout.table.adm] = 0
+        ranks = torch.from_numpy(np.tile(r, nrep)).cuda()
+        return cls(layout, values, ranks)
+
+    def instance(self, b: int):
+        """View of instance b of a batched store."""
+        sz, nb = self.layout.size, self.table.n
+        return HStore(self.layout, self.values[b * sz:(b + 1) * sz], self.ranks[b * nb:(b + 1) * nb])
+
     def copy_from(self, other: "HStore"):
         self.values.copy_(other.values)
         self.ranks.copy_(other.ranks)
@@ -130,7 +145,7 @@ class ExecPlan:
     """Lowered H-LU plan + its device execution graph."""
 
     def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
-                 sparsify=False, max_ctas=0):
+                 sparsify=False, max_ctas=0, nrep=1):
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
         self.table = table
@@ -150,17 +165,33 @@ class ExecPlan:
         ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()
         self.succ_ptr, self.succ_idx = ptr, idx
         lv = tg.asap_levels(len(prog.keys), ptr, idx)
+        self.levels = lv
+        self.n_tasks = len(prog.keys)
+        self.nrep = int(nrep)
+        ops, task_ops = prog.ops, prog.task_ops
+        if self.nrep > 1:
+            # disjoint union of nrep copies: batched same-structure instances
+            from .planner import replicate
+
+            nb = table.n
+            lay = self.layout
+            ops, task_ops, _ = replicate(prog, self.nrep,
+                                         {0: lay.size, 1: lay.size, 2: lay.size, 3: prog.acc_size},
+                                         {0: nb, 1: nb, 2: nb, 3: nb})
+            nt, ne = self.n_tasks, len(idx)
+            ptr = np.concatenate([ptr[:-1] + b * ne for b in range(self.nrep)] +
+                                 [[ne * self.nrep]]).astype(np.int32)
+            idx = np.concatenate([idx + b * nt for b in range(self.nrep)]).astype(np.int32)
+            lv = np.tile(lv, self.nrep)
         order = np.argsort(lv, kind="stable").astype(np.int32)
         counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
-        self.levels = lv
         self.wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.wave_tasks = order
-        self.n_tasks = len(prog.keys)
-        self.plan = _lib.Plan(prog.ops, prog.task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
+        self.plan = _lib.Plan(ops, task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
                               prog.scratch_doubles, prog.scratch_ranks, max_ctas)
         torch = _torch()
-        self.acc_values = torch.zeros(prog.acc_size, dtype=torch.float64, device="cuda")
-        self.acc_ranks = torch.zeros(max(table.n, 1), dtype=torch.int32, device="cuda")
+        self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
+        self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")
         self.plan.bind(ACC_BASE_ID, self.acc_values, self.acc_ranks)
 
     def _exec_graph(self):
@@ -216,8 +247,10 @@ class ExecPlan:
 
     def bind(self, A: HStore, L: HStore, U: HStore):
         for i, s in enumerate((A, L, U)):
-            if s.layout.table is not self.table:
+            if s.layout.table is not self.table and s.layout.table.n != self.table.n:
                 raise ValueError("operand is not over the plan's block tree")
+            if s.values.numel() < self.layout.size * self.nrep:
+                raise ValueError("operand storage smaller than the plan's batch")
             if (s.layout.u_off != self.layout.u_off).any() or (s.layout.d_off != self.layout.d_off).any():
                 raise ValueError("operand storage layout differs from the plan's")
             self.plan.bind(i, s.values, s.ranks)
@@ -242,7 +275,7 @@ class ExecPlan:
     def counters(self, stream=None):
         c = self.plan.counters(stream)
         return {"truncations": c[0], "flops": c[1], "bytes": c[2], "tasks": c[3],
-                "updates": self.prog.updates}
+                "updates": self.prog.updates * self.nrep}
 
     def stats(self):
         w = np.diff(self.wave_ptr)

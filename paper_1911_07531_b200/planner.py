@@ -901,3 +901,47 @@ def plan_hlu(table: BlockTable, mode: str, policy, rank_cap=None):
     prog = p.pack()
     prog.layout = lay
     return prog
+
+
+def replicate(prog, nrep, base_sizes, slot_sizes):
+    """Disjoint union of ``nrep`` copies of a program (batched instances).
+
+    Copy b's matrix refs of base i are shifted by b * base_sizes[i] elements
+    and its rank slots of base i by b * slot_sizes[i]; scratch refs (base
+    15) are per-CTA and stay.  Used for batches of same-structure instances
+    (config 4: 256 HODLR matrices share one block tree).
+    """
+    ops = prog.ops
+    n = len(ops)
+    out = np.tile(ops, nrep)
+    rep = np.repeat(np.arange(nrep, dtype=np.int64), n)
+    mask56 = (1 << 56) - 1
+    for field in ("ref", "wref"):
+        r = out[field]
+        r2 = r.reshape(len(out), -1)
+        base = (r2.astype(np.uint64) >> np.uint64(56)).astype(np.int64)
+        off = r2 & mask56
+        shift = np.zeros_like(off)
+        for b, sz in base_sizes.items():
+            sel = base == b
+            shift[sel] = (rep[:, None] * int(sz) * np.ones_like(off))[sel]
+        newv = (base << 56) | (off + shift)
+        out[field] = newv.reshape(out[field].shape)
+    s = out["slot"]
+    d = out["dim"]
+    for arr in (s, d):
+        neg = arr < 0
+        code = -arr - 1
+        b = code >> 24
+        idx = code & 0xFFFFFF
+        add = np.zeros_like(arr)
+        for bb, sz in slot_sizes.items():
+            sel = neg & (b == bb)
+            add[sel] = (rep[:, None] * int(sz) * np.ones_like(arr))[sel]
+        newcode = (b << 24) | (idx + add)
+        arr[neg] = (-(newcode + 1))[neg]
+    task_ops = prog.task_ops
+    nt = len(task_ops) - 1
+    t_all = (task_ops[None, :-1] + (np.arange(nrep)[:, None] * n)).ravel()
+    new_task_ops = np.concatenate([t_all, [n * nrep]]).astype(np.int64)
+    return out, new_task_ops, nt
