@@ -1,0 +1,48 @@
+"""The C-ABI library loads on a CPU-only machine and exports every entry
+point declared in include/hmx.h (no compute calls without a GPU)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1911_07531_b200 import _build, _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared():
+    hdr = open(os.path.join(ROOT, "include", "hmx.h")).read()
+    return sorted(set(re.findall(r"\b(hmx_[a-z0-9_]+)\s*\(", hdr)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return ctypes.CDLL(_build.LIB)
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared()
+    assert len(names) >= 15
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_table_matches_header():
+    assert sorted(_lib.EXPORTED) == declared()
+
+
+def test_version_and_record_size(lib):
+    L = _lib.lib()
+    assert L.hmx_version().startswith(b"hmx")
+    assert L.hmx_op_size() == 128 == _lib.OP_DTYPE.itemsize
+
+
+def test_sm100a_code_in_library():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _build.LIB],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
