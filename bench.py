@@ -190,6 +190,14 @@ def oracle_sample(cfg, A_leaves, depth):
     return O, bt, u, lv
 
 
+_JOB = None
+
+
+def _oracle_job(_i):
+    """Pool worker: one sample factorization of the forked-in job."""
+    return _oracle_run(_JOB)
+
+
 def _oracle_run(args):
     O, bt, u, lv, mode, pol = args
     from threadpoolctl import threadpool_limits
@@ -252,15 +260,16 @@ def run_reference(args):
     opol = O.Policy("accuracy", eps=cfg.eps)
     ncores = len(os.sched_getaffinity(0))
     nproc = max(1, min(ncores, 32))
+    global _JOB
+    _JOB = (O, bt, u, lv, cfg.mode, opol)
     ctx = mp.get_context("fork")
-    job = (O, bt, u, lv, cfg.mode, opol)
     with ctx.Pool(nproc) as pool:
         for _ in range(args.warmup):
-            pool.map(_oracle_run, [job] * nproc)
+            pool.map(_oracle_job, range(nproc))
         t0 = time.perf_counter()
         flops = 0.0
         for _ in range(args.steps):
-            res = pool.map(_oracle_run, [job] * nproc)
+            res = pool.map(_oracle_job, range(nproc))
             flops += sum(r[1] for r in res)
         wall = time.perf_counter() - t0
     value = flops / wall / 1e9

@@ -264,6 +264,29 @@ __device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau
   }
 }
 
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Householder QR by a group of nw warps [wbeg, wbeg + nw) synchronised on
+// named barrier bar_id, so that two factorizations (U and V of a
+// truncation) run concurrently in one CTA.
+__device__ void group_householder_qr(int m, int K, double* A, int lda, double* tau, int wbeg,
+                                     int nw, int bar_id) {
+  const int p = min(m, K);
+  const int w = (int)(threadIdx.x >> 5) - wbeg;
+  for (int j = 0; j < p; ++j) {
+    double* x = A + (int64_t)j * lda;
+    if (w == 0) warp_reflector(m, j, x, tau);
+    named_bar(bar_id, nw * 32);
+    const double t = tau[j];
+    if (t != 0.0)
+      for (int c = j + 1 + w; c < K; c += nw)
+        warp_apply_reflector(m, j, x, t, A + (int64_t)c * lda);
+    named_bar(bar_id, nw * 32);
+  }
+}
+
 // X (m x r) := Q X where Q = H_0 H_1 ... H_{p-1} from cta_householder_qr.
 // Columns of X are independent: one warp per column, no block barriers.
 __device__ void cta_apply_q(int m, int p, const double* A, int lda, const double* tau, int r,
@@ -399,11 +422,14 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
 // Rank-revealing QR: column-pivoted Householder QR (LAPACK dgeqp3 / dlaqp2
 // conventions) of the p x q matrix G, stopped after k steps as soon as the
 // Frobenius norm of the trailing block G[k:, k:] is <= thr * |R_00|.
-// |R_00| (the largest column norm) is a lower bound of sigma_1, so dropping
-// the trailing block moves every singular value by at most thr*sigma_1
-// (Weyl); the callers use thr = 1e-8 * (keep cut), far below the measured
-// rank margins (SURVEY.md finding 4).  Returns k; perm[c] = original column
-// of pivoted column c; tau[j] the reflector scalars; R in rows 0..k-1.
+// Dropping the trailing rows B = [0 R22] of R is a positive semidefinite
+// change of R^T R = A^T A + B^T B, so every singular value moves by at most
+// ||B||^2 / sigma_i <= thr^2 sigma_1^2 / sigma_i (|R_00| <= sigma_1).  The
+// callers use thr = 1e-5 * cut: singular values at the keep cut
+// (cut * sigma_1) move by <= 1e-10 relative, far below the measured rank
+// margins (>= 4e-5 relative, SURVEY.md finding 4).  Returns k; perm[c] =
+// original column of pivoted column c; tau[j] the reflector scalars; R in
+// rows 0..k-1.
 // Per step: warp 0 pivots, swaps and builds the reflector (one barrier),
 // all warps apply it and downdate column norms (one barrier).
 // ---------------------------------------------------------------------------

@@ -116,7 +116,7 @@ __device__ __forceinline__ double svd_flops(double m, double n) {
 // ---------------------------------------------------------------------------
 // low-rank SVD of a dense p x q block G (destroyed):
 //   rank-revealing QR (stopped once the trailing block is below
-//   1e-8 * cut * sigma_1), then one-sided Jacobi on the k x q factor R1^T
+//   1e-5 * cut * sigma_1, see cta_rrqr), then one-sided Jacobi on R1^T
 //   (QR-preconditioned, so few sweeps), sorted singular values, keep.
 // Writes dstU (p x r) = W_r Sigma_r and dstV (q x r) = Z_r, G ~ dstU dstV^T.
 // ws: >= 6q + 2q^2 doubles.  smw/smcap: shared work area for X and J.
@@ -142,7 +142,10 @@ __device__ __forceinline__ void phase(const DevPlan& P, int slot, unsigned long 
 
 __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, double* G, int ldg,
                            double* ws, double* smw, int smcap, double* dstU, int ldu,
-                           double* dstV, int ldv, double* sm, double* sig_out = nullptr) {
+                           double* dstV, int ldv, double* sm, double* sig_out = nullptr,
+                           double* gevict = nullptr, int ldevict = 0, double* smfull = nullptr,
+                           int smfullcap = 0, double** defer_g = nullptr, int* defer_ld = nullptr,
+                           double** defer_tau = nullptr, int* defer_k = nullptr) {
   double* red = sm;
   int* ired = reinterpret_cast<int*>(sm + 16);
   int* flag = reinterpret_cast<int*>(sm + 24);
@@ -155,11 +158,21 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   double* rest = ws + 6 * q;
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
-  const double thr = sig_out ? 0.0 : 1e-8 * cut;
+  const double thr = sig_out ? 0.0 : 1e-5 * cut;  // see cta_rrqr
   unsigned long long t0 = P.trace ? gtimer2() : 0;
   const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
   phase(P, 13, t0);
   double *X, *J;
+  if (q * k + k * k > smcap && gevict && q * k + k * k <= smfullcap) {
+    // the Jacobi factors matter more than G: move G (R + reflectors) out of
+    // shared memory and give the whole work area to X and J
+    FOR_MN(i, c, p, q) gevict[i + (int64_t)c * ldevict] = G[i + (int64_t)c * ldg];
+    __syncthreads();
+    G = gevict;
+    ldg = ldevict;
+    smw = smfull;
+    smcap = smfullcap;
+  }
   if (q * k + k * k <= smcap) { X = smw; J = smw + q * k; }
   else { X = rest; J = rest + (int64_t)q * k; }
   FOR_MN(c, i, q, k) X[c + i * q] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
@@ -189,6 +202,13 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
     dstV[perm[c] + (int64_t)t * ldv] = X[c + col * q] / sig[col];
   }
   __syncthreads();
+  if (defer_g) {  // the caller fuses Q_G into its own recomposition
+    *defer_g = G;
+    *defer_ld = ldg;
+    *defer_tau = tau;
+    *defer_k = k;
+    return r;
+  }
   cta_apply_q(p, k, G, ldg, tau, r, dstU, ldu);
   return r;
 }
@@ -247,8 +267,12 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     __syncthreads();
     U = Us;
     V = Vs;
-    cta_householder_qr(m, K, U, m, tau_u, red);
-    cta_householder_qr(n, K, V, n, tau_v, red);
+    // QR(U) on warps 0-3 and QR(V) on warps 4-7, concurrently
+    if ((threadIdx.x >> 5) < HMX_WARPS / 2)
+      group_householder_qr(m, K, U, m, tau_u, 0, HMX_WARPS / 2, 1);
+    else
+      group_householder_qr(n, K, V, n, tau_v, HMX_WARPS / 2, HMX_WARPS / 2, 2);
+    __syncthreads();
     FOR_MN(i, j, p, q) {
       double acc = 0.0;
       for (int l = max(i, j); l < K; ++l) acc = fma(U[i + l * m], V[j + l * n], acc);
@@ -274,14 +298,40 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   }
   const int ldu_q = stage ? m : ldu, ldv_q = stage ? n : ldv;
   phase(P, 12, tq);
-  const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm);
+  double* Gq = nullptr;
+  double* tau_g = nullptr;
+  int ldgq = 0, kg = 0;
+  const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm, nullptr,
+                            (!stage && G != Gg) ? Gg : nullptr, p, work, kSmemWork,
+                            stage ? &Gq : nullptr, &ldgq, &tau_g, &kg);
   if (P.trace && threadIdx.x == 0) tq = gtimer2();
   FOR_MN(i, t, m - p, r) Uo[p + i + (int64_t)t * lduo] = 0.0;
   FOR_MN(i, t, n - q, r) Vo[q + i + (int64_t)t * ldvo] = 0.0;
   __syncthreads();
   if (stage) {
-    cta_apply_q(m, p, U, ldu_q, tau_u, r, Uo, lduo);
-    cta_apply_q(n, q, V, ldv_q, tau_v, r, Vo, ldvo);
+    // fused recomposition: U columns get Q_G then Q_u, V columns Q_v; one
+    // warp per column job, no block barriers between reflectors
+    const int w = threadIdx.x >> 5;
+    for (int job = w; job < 2 * r; job += HMX_WARPS) {
+      if (job < r) {
+        double* y = Uo + (int64_t)job * lduo;
+        for (int j = kg - 1; j >= 0; --j) {
+          const double t = tau_g[j];
+          if (t != 0.0) warp_apply_reflector(p, j, Gq + (int64_t)j * ldgq, t, y);
+        }
+        for (int j = p - 1; j >= 0; --j) {
+          const double t = tau_u[j];
+          if (t != 0.0) warp_apply_reflector(m, j, U + (int64_t)j * ldu_q, t, y);
+        }
+      } else {
+        double* y = Vo + (int64_t)(job - r) * ldvo;
+        for (int j = q - 1; j >= 0; --j) {
+          const double t = tau_v[j];
+          if (t != 0.0) warp_apply_reflector(n, j, V + (int64_t)j * ldv_q, t, y);
+        }
+      }
+    }
+    __syncthreads();
   } else {
     cta_apply_q_blocked(m, p, Vxu, m, Tu, r, Uo, lduo, Wq, work, kSmemWork);
     cta_apply_q_blocked(n, q, Vxv, n, Tv, r, Vo, ldvo, Wq, work, kSmemWork);
@@ -318,7 +368,8 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   }
   double* smw = gsm ? work + m * n : work;
   const int smcap = gsm ? kSmemWork - m * n : kSmemWork;
-  const int r = svd_lowrank(P, o, m, n, G, ldg, ws, smw, smcap, Uo, o.ld[2], Vo, o.ld[3], sm);
+  const int r = svd_lowrank(P, o, m, n, G, ldg, ws, smw, smcap, Uo, o.ld[2], Vo, o.ld[3], sm,
+                            nullptr, gsm ? M : nullptr, ldm, work, kSmemWork);
   if (threadIdx.x == 0) *rslot = r;
   const int s = min(m, n);
   count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s + (double)s * n));

@@ -2,7 +2,9 @@
 
 Tolerances: the kernels are fp64; products and solves are compared at
 1e-12 relative, LU at bitwise equality (the device LU mirrors
-arith.dense_lu's rounding: separate multiply and subtract, arith.py:70-71).
+arith.dense_lu's rounding: separate multiply and subtract, arith.py:70-71),
+truncation ranks exactly and recompressed products within
+max(1e-10, 1e-3*eps) relative (tolerance tied to the truncation eps).
 """
 
 import numpy as np
@@ -105,13 +107,14 @@ def test_truncate_vs_reference_fixtures():
             assert Un.shape[1] == int(ref[f"t{i}_{eps:g}_rank"]), (i, eps)
             pr = ref[f"t{i}_{eps:g}_probe"]
             got = Un @ (Vn.T @ probe_vec(n))
-            assert np.linalg.norm(got - pr) <= 1e-10 * np.linalg.norm(pr) + 1e-13
+            # the rank-revealing step drops a tail <= 1e-5*eps*sigma_1 (see cta_rrqr)
+            assert np.linalg.norm(got - pr) <= max(1e-10, 1e-3 * eps) * np.linalg.norm(pr) + 1e-13
         for eps in (1e-4, 1e-6):
             W, Z = kernels.dense_to_lowrank(M, _Pol("accuracy", eps=eps))
             assert W.shape[1] == int(ref[f"d{i}_{eps:g}_rank"]), (i, eps)
             pr = ref[f"d{i}_{eps:g}_probe"]
             got = W @ (Z.T @ probe_vec(n))
-            assert np.linalg.norm(got - pr) <= 1e-10 * np.linalg.norm(pr) + 1e-13
+            assert np.linalg.norm(got - pr) <= max(1e-10, 1e-3 * eps) * np.linalg.norm(pr) + 1e-13
 
 
 def test_truncate_policies_and_passthrough():

@@ -81,3 +81,8 @@ for t in path:
     for o in ops[plan.prog.task_ops[t]:plan.prog.task_ops[t + 1]]:
         oc[int(o["code"])] += 1
 print("  ops on path", dict(oc))
+pd = sorted(path, key=lambda t: -dur[t])[:25]
+for t in pd:
+    o = ops[plan.prog.task_ops[t]:plan.prog.task_ops[t + 1]]
+    tr = [(int(x["dim"][0]), int(x["dim"][1])) for x in o if x["code"] in (8, 9)]
+    print(f"  path task {plan.prog.keys[t]} {dur[t]:.0f}us ops={len(o)} trunc/d2lr={tr}")
