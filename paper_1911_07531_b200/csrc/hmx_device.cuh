@@ -72,17 +72,19 @@ __device__ void cta_add(int m, int n, double alpha, const double* A, int lda, do
 // smem: 2*16*65 doubles.
 // ---------------------------------------------------------------------------
 constexpr int GT = 64, GK = 16, GPAD = 65;
-constexpr int GEMM_SMEM_DOUBLES = 2 * GK * GPAD;
+constexpr int GEMM_SMEM_DOUBLES = 4 * GK * GPAD;  // two stages of A and B tiles
 
+// k-chunks are double buffered: the global loads of chunk c+1 are issued
+// into registers before the FMAs of chunk c, so the L2/HBM latency of the
+// operand stream overlaps the arithmetic (one barrier per chunk).
 __device__ void cta_gemm(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
                          bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
                          double* C, int ldc, double* sm) {
   if (m <= 0 || n <= 0) return;
-  double* As = sm;              // [GK][GPAD] : As[kk*GPAD + i]
-  double* Bs = sm + GK * GPAD;  // [GK][GPAD] : Bs[kk*GPAD + j]
   const int tid = threadIdx.x;
   const int tr = tid & 15, tc = tid >> 4;
   const int tiles_m = (m + GT - 1) / GT, tiles_n = (n + GT - 1) / GT;
+  constexpr int NL = (GT * GK) / HMX_THREADS;  // elements of each tile per thread
   for (int tile = 0; tile < tiles_m * tiles_n; ++tile) {
     const int m0 = (tile % tiles_m) * GT, n0 = (tile / tiles_m) * GT;
     double acc[4][4];
@@ -90,26 +92,46 @@ __device__ void cta_gemm(int m, int n, int k, double alpha, const double* __rest
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    for (int k0 = 0; k0 < k; k0 += GK) {
-      __syncthreads();
+    double ra[NL], rb[NL];
+    auto load = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < (GT * GK) / HMX_THREADS; ++q) {
+      for (int q = 0; q < NL; ++q) {
         const int e = tid + q * HMX_THREADS;
         int i, kk;
         if (!ta) { i = e % GT; kk = e / GT; } else { kk = e % GK; i = e / GK; }
         const int gi = m0 + i, gk = k0 + kk;
-        double v = 0.0;
-        if (gi < m && gk < k) v = ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda];
-        As[kk * GPAD + i] = v;
+        ra[q] = (gi < m && gk < k) ? (ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda])
+                                   : 0.0;
         int j, kb;
         if (!tb) { kb = e % GK; j = e / GK; } else { j = e % GT; kb = e / GT; }
         const int gj = n0 + j, gkb = k0 + kb;
-        double w = 0.0;
-        if (gj < n && gkb < k) w = tb ? B[gj + (int64_t)gkb * ldb] : B[gkb + (int64_t)gj * ldb];
-        Bs[kb * GPAD + j] = w;
+        rb[q] = (gj < n && gkb < k) ? (tb ? B[gj + (int64_t)gkb * ldb] : B[gkb + (int64_t)gj * ldb])
+                                    : 0.0;
       }
-      __syncthreads();
-      const int kc = min(GK, k - k0);
+    };
+    auto store = [&](int buf) {
+      double* As = sm + buf * 2 * GK * GPAD;
+      double* Bs = As + GK * GPAD;
+#pragma unroll
+      for (int q = 0; q < NL; ++q) {
+        const int e = tid + q * HMX_THREADS;
+        int i, kk;
+        if (!ta) { i = e % GT; kk = e / GT; } else { kk = e % GK; i = e / GK; }
+        As[kk * GPAD + i] = ra[q];
+        int j, kb;
+        if (!tb) { kb = e % GK; j = e / GK; } else { j = e % GT; kb = e / GT; }
+        Bs[kb * GPAD + j] = rb[q];
+      }
+    };
+    const int nk = (k + GK - 1) / GK;
+    load(0);
+    store(0);
+    __syncthreads();
+    for (int c = 0; c < nk; ++c) {
+      if (c + 1 < nk) load((c + 1) * GK);
+      const double* As = sm + (c & 1) * 2 * GK * GPAD;
+      const double* Bs = As + GK * GPAD;
+      const int kc = min(GK, k - c * GK);
       for (int kk = 0; kk < kc; ++kk) {
         double a[4], b[4];
 #pragma unroll
@@ -121,6 +143,8 @@ __device__ void cta_gemm(int m, int n, int k, double alpha, const double* __rest
 #pragma unroll
           for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
       }
+      if (c + 1 < nk) store((c + 1) & 1);
+      __syncthreads();
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -130,8 +154,8 @@ __device__ void cta_gemm(int m, int n, int k, double alpha, const double* __rest
       for (int i = 0; i < 4; ++i) {
         const int gi = m0 + tr + 16 * i;
         if (gi >= m) continue;
-        double* c = C + gi + (int64_t)gj * ldc;
-        *c = beta1 ? (*c + alpha * acc[i][j]) : alpha * acc[i][j];
+        double* cp = C + gi + (int64_t)gj * ldc;
+        *cp = beta1 ? (*cp + alpha * acc[i][j]) : alpha * acc[i][j];
       }
     }
   }
