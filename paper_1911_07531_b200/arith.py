@@ -25,13 +25,14 @@ class SingularPivotError(RuntimeError):
 _PLANS = {}
 
 
-def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0):
+def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0,
+             split_min=engine.DEFAULT_SPLIT_MIN):
     """Cached execution plan (planning and upload happen once per tree)."""
-    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas)
+    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min)
     p = _PLANS.get(key)
     if p is None or p.table is not table:
         p = engine.ExecPlan(table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify,
-                            max_ctas=max_ctas)
+                            max_ctas=max_ctas, split_min=split_min)
         _PLANS[key] = p
     return p
 
@@ -55,13 +56,13 @@ def _check_operands(*ms):
 
 
 def run_hlu(A, L, U, policy, mode, exec_mode=engine.EXEC_PERSISTENT, dag_mode=None,
-            sparsify=False, stream=None):
+            sparsify=False, stream=None, split_min=engine.DEFAULT_SPLIT_MIN):
     t = _check_operands(A, L, U)
     rc = A.store.layout.rank_cap
     for M in (L, U):
         if M.store.layout.rank_cap != rc:
             raise ValueError("L/U storage rank_cap differs from A's")
-    plan = get_plan(t, mode, policy, rc, dag_mode, sparsify)
+    plan = get_plan(t, mode, policy, rc, dag_mode, sparsify, split_min=split_min)
     plan.run(A.store, L.store, U.store, exec_mode, stream)
     c = plan.counters(stream)
     counters.add(c["truncations"], c["updates"])

@@ -23,6 +23,9 @@ from .planner import ACC_BASE_ID, Layout, dataflow_edges, plan_hlu
 from .trees import BlockTable
 
 EXEC_WAVE, EXEC_GRAPH, EXEC_PERSISTENT, EXEC_SEQUENTIAL = 0, 1, 2, 3
+WS_BASE_ID = 5
+# H x H products with min(m, n) >= this are split into parallel micro-tasks
+DEFAULT_SPLIT_MIN = 256
 
 
 def _torch():
@@ -145,14 +148,14 @@ class ExecPlan:
     """Lowered H-LU plan + its device execution graph."""
 
     def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
-                 sparsify=False, max_ctas=0, nrep=1):
+                 sparsify=False, max_ctas=0, nrep=1, split_min=DEFAULT_SPLIT_MIN):
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
         self.table = table
         self.mode = mode
         self.policy = policy
         self.rank_cap = rank_cap
-        prog = plan_hlu(table, mode, policy, rank_cap)
+        prog = plan_hlu(table, mode, policy, rank_cap, split_min=split_min)
         self.prog = prog
         self.layout = prog.layout
         dag_mode = dag_mode or ("std" if mode == "std" else tg.MERGED)
@@ -176,8 +179,9 @@ class ExecPlan:
             nb = table.n
             lay = self.layout
             ops, task_ops, _ = replicate(prog, self.nrep,
-                                         {0: lay.size, 1: lay.size, 2: lay.size, 3: prog.acc_size},
-                                         {0: nb, 1: nb, 2: nb, 3: nb})
+                                         {0: lay.size, 1: lay.size, 2: lay.size, 3: prog.acc_size,
+                                          WS_BASE_ID: prog.ws_size},
+                                         {0: nb, 1: nb, 2: nb, 3: nb, WS_BASE_ID: prog.ws_slots})
             nt, ne = self.n_tasks, len(idx)
             ptr = np.concatenate([ptr[:-1] + b * ne for b in range(self.nrep)] +
                                  [[ne * self.nrep]]).astype(np.int32)
@@ -193,6 +197,9 @@ class ExecPlan:
         self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")
         self.plan.bind(ACC_BASE_ID, self.acc_values, self.acc_ranks)
+        self.ws_values = torch.zeros(prog.ws_size * self.nrep, dtype=torch.float64, device="cuda")
+        self.ws_ranks = torch.zeros(prog.ws_slots * self.nrep, dtype=torch.int32, device="cuda")
+        self.plan.bind(WS_BASE_ID, self.ws_values, self.ws_ranks)
 
     def _exec_graph(self):
         """Successor CSR over program tasks (program order = trace order).
@@ -207,7 +214,11 @@ class ExecPlan:
         """
         prog = self.prog
         pos = {}
+        micro = set()
         for i, k in enumerate(prog.keys):
+            if k[0] == "micro":
+                micro.add(i)
+                continue
             if k in pos:
                 raise RuntimeError(f"duplicate planned task {k}")
             pos[k] = i
@@ -225,9 +236,26 @@ class ExecPlan:
             a = dag_to_prog[i]
             for j in didx[dptr[i]:dptr[i + 1]]:
                 dag_edges.add((a, dag_to_prog[j]))
+        groups = getattr(prog, "groups", {})
         if self.mode == "std":
-            edges = dag_edges
-            n_extra = 0
+            edges = set(dag_edges)
+            # a DAG task's predecessors also precede its micro-tasks; the
+            # micro-tasks feed the task through the plan workspace
+            for a, b in dag_edges:
+                for mtask in groups.get(b, ()):
+                    edges.add((a, mtask))
+            if micro:
+                root_of = {}
+                for r, ms in groups.items():
+                    for mtask in ms:
+                        root_of[mtask] = r
+                tables = {b: self.table for b in range(4)}
+                for a, b in dataflow_edges(prog, tables):
+                    ga = root_of.get(a, a)
+                    gb = root_of.get(b, b)
+                    if ga == gb:
+                        edges.add((a, b))
+            n_extra = len(edges - dag_edges)
         else:
             tables = {b: self.table for b in range(4)}
             edges = dataflow_edges(prog, tables)

@@ -37,6 +37,7 @@ from ._lib import (F_ACC, F_TA, F_TB, OP_ADD, OP_APPEND, OP_COPY, OP_D2LR, OP_GE
 from .trees import BlockTable
 
 ACC_BASE_ID = 3
+WS_BASE_ID = 5
 ALIGN = 4  # doubles (32 B)
 
 
@@ -167,14 +168,23 @@ class Program:
 class Planner:
     """Symbolic executor of the reference recursions; emits op programs."""
 
-    def __init__(self, policy, rank_cap=None):
+    def __init__(self, policy, rank_cap=None, split_min=0):
         self.mode, self.kfix, self.eps = _policy_fields(policy)
         self.rank_cap = rank_cap
-        self.ops = []
-        self.task_start = []
+        # tasks: op lists, program order (micro-tasks are placed before the
+        # task that consumes their results), current task id
+        self.task_lists = []
+        self.order = []
+        self.cur = None
+        self.cur_id = -1
         self.keys = []
         self.kinds = []
-        self.cur = None
+        self.groups = {}
+        # plan workspace (base WS_BASE_ID): results of micro-tasks
+        self.split_min = int(split_min)
+        self.wtop = 0
+        self.wslots = 0
+        self.nw = 0
         self.top = self.peak = 0
         self.peak_task = -1
         self.rtop = self.rpeak = 0
@@ -189,36 +199,92 @@ class Planner:
         self.acc_table = None
         # per-task data access: reads (objects or subtrees) and writes
         self.rw = []
+        self._root_of = {}
+        self.pre = {}
 
     # ------------------------------------------------------------------
     # op emission
     # ------------------------------------------------------------------
     def _op(self, code, flags=0, dims=(0, 0, 0, 0), lds=(0, 0, 0, 0), refs=(None,) * 4,
             slots=(0, 0, 0, 0), iargs=(0, 0, 0, 0), fargs=(0.0, 0.0), wref=None):
-        self.ops.append((code, flags, dims, lds, refs, slots, iargs, fargs, wref))
+        self.cur.append((code, flags, dims, lds, refs, slots, iargs, fargs, wref))
 
-    def begin(self, kind, key):
-        self.task_start.append(len(self.ops))
+    def _new_task(self, kind, key):
+        tid = len(self.task_lists)
+        self.task_lists.append([])
         self.kinds.append(kind)
         self.keys.append(key)
         self.rw.append(([], []))
+        self.cur = self.task_lists[tid]
+        self.cur_id = tid
         self.top = 0
         self.rtop = 0
+        return tid
+
+    def begin(self, kind, key):
+        tid = self._new_task(kind, key)
+        self.order.append(tid)
 
     # data-access records: ("m", base, uid) = every leaf of the subtree of
-    # uid in matrix `base`; ("a", uid) = accumulator of block uid
+    # uid in matrix `base`; ("a", uid) = accumulator of block uid;
+    # ("w", id) = a micro-task result in the plan workspace
     def _rd(self, obj):
-        self.rw[-1][0].append(obj)
+        self.rw[self.cur_id][0].append(obj)
 
     def _wr(self, obj):
-        self.rw[-1][1].append(obj)
+        self.rw[self.cur_id][1].append(obj)
+
+    # ------------------------------------------------------------------
+    # micro-tasks: a large H x H product is split into its 8 independent
+    # quadrant products, each run by its own CTA; results go to the plan
+    # workspace and the consuming task (placed after them in program order)
+    # combines them.  Parallelism inside a DAG task, same arithmetic.
+    # ------------------------------------------------------------------
+    def _wref(self, rows, cols):
+        off = self.wtop
+        self.wtop += _al(max(rows * max(cols, 1), 1))
+        return Ref(WS_BASE_ID, off, max(rows, 1))
+
+    def _wslot(self):
+        s = self.wslots
+        self.wslots += 1
+        return L.slot(WS_BASE_ID, s)
+
+    def _micro_product(self, alpha, X, ua, Y, ub, depth):
+        parent = (self.cur, self.cur_id, self.top, self.rtop)
+        pkey = self.keys[self.cur_id]
+        tid = self._new_task("micro_product", ("micro", pkey, ua, ub))
+        self.pre.setdefault(parent[1], []).append(tid)
+        self.groups.setdefault(self._group_root(parent[1]), []).append(tid)
+        self._root_of[tid] = self._group_root(parent[1])
+        q = self.product(alpha, X, ua, Y, ub, depth + 1)
+        wid = self.nw
+        self.nw += 1
+        if q.kind == "D":
+            W = self._wref(q.m, q.n)
+            self.copy(q.m, q.n, 1.0, q.ref, W)
+            out = PD(W, q.m, q.n)
+        else:
+            Wu, Wv = self._wref(q.m, q.kmax), self._wref(q.n, q.kmax)
+            ws = self._wslot()
+            self.copy(q.m, q.k, 1.0, q.U, Wu)
+            self.copy(q.n, q.k, 1.0, q.V, Wv)
+            self.setrank(ws, q.k)
+            out = PR(Wu, Wv, q.m, q.n, ws, q.kmax)
+        self._wr(("w", wid))
+        self.cur, self.cur_id, self.top, self.rtop = parent
+        self._rd(("w", wid))
+        return out
+
+    def _group_root(self, tid):
+        return self._root_of.get(tid, tid)
 
     def alloc(self, n):
         off = self.top
         self.top += _al(max(int(n), 1))
         if self.top > self.peak:
             self.peak = self.top
-            self.peak_task = len(self.keys) - 1
+            self.peak_task = self.cur_id
         return off
 
     def sref(self, rows, cols):
@@ -353,7 +419,7 @@ class Planner:
     # ------------------------------------------------------------------
     # product payloads (hmatrix.py:367-417)
     # ------------------------------------------------------------------
-    def product(self, alpha, X: PMat, ua, Y: PMat, ub):
+    def product(self, alpha, X: PMat, ua, Y: PMat, ub, depth=0):
         self._rd(("m", X.base, ua))
         self._rd(("m", Y.base, ub))
         tx, ty = X.t, Y.t
@@ -388,7 +454,10 @@ class Planner:
             S = self.sref(kk, n)
             self.copy(kk, n, alpha, Y.dense(ub), S)
             return PD(self.hm_apply(X, ua, S, n, n), m, n)
-        # both blocked: combine the 2x2x2 quadrant payloads
+        # both blocked: combine the 2x2x2 quadrant payloads; large products
+        # run their quadrants as parallel micro-tasks
+        split = (self.split_min > 0 and depth < 2 and min(m, n) >= self.split_min
+                 and not (tx.leaf[tx.child(ua, 0, 0)] and ty.leaf[ty.child(ub, 0, 0)]))
         parts = []
         dacc = None
         for i in range(2):
@@ -396,7 +465,10 @@ class Planner:
                 for l in range(2):
                     a_il = tx.child(ua, i, l)
                     b_lj = ty.child(ub, l, j)
-                    q = self.product(alpha, X, a_il, Y, b_lj)
+                    if split:
+                        q = self._micro_product(alpha, X, a_il, Y, b_lj, depth)
+                    else:
+                        q = self.product(alpha, X, a_il, Y, b_lj, depth + 1)
                     r0 = int(tx.r0[a_il] - tx.r0[ua])
                     c0 = int(ty.c0[b_lj] - ty.c0[ub])
                     if q.kind == "D":
@@ -609,7 +681,7 @@ class Planner:
         self.acc_need_lr[u] = max(self.acc_need_lr.get(u, 0), int(k), self._acc_cap(u))
 
     def _chain(self, u):
-        self.fold_chains.setdefault(u, []).append(len(self.keys) - 1)
+        self.fold_chains.setdefault(u, []).append(self.cur_id)
 
     def acc_fold(self, u, p):
         """Accumulator.fold (accumulator.py:60-76) into acc(u)."""
@@ -799,6 +871,27 @@ class Planner:
         def iv(x):
             return int(x.fn()) if isinstance(x, _Lazy) else int(x)
 
+        # program order: micro-tasks before their consumers
+        order = []
+        stack = []
+        for t in self.order:
+            # iterative post-order over the micro-task tree of t
+            stack.append((t, False))
+            while stack:
+                x, done = stack.pop()
+                if done:
+                    order.append(x)
+                    continue
+                stack.append((x, True))
+                for c in reversed(self.pre.get(x, [])):
+                    stack.append((c, False))
+        newidx = {t: i for i, t in enumerate(order)}
+        flat = []
+        starts = []
+        for t in order:
+            starts.append(len(flat))
+            flat.extend(self.task_lists[t])
+        self.ops = flat
         n = len(self.ops)
         arr = np.zeros(n, dtype=L.OP_DTYPE)
         code = np.empty(n, np.int32)
@@ -823,15 +916,18 @@ class Planner:
         arr["code"], arr["flags"], arr["dim"], arr["ld"] = code, flags, dims, lds
         arr["ref"], arr["slot"], arr["iarg"], arr["farg"], arr["wref"] = refs, slots, iargs, fargs, wref
         prog.ops = arr
-        prog.task_ops = np.asarray(self.task_start + [n], dtype=np.int64)
-        prog.keys = list(self.keys)
-        prog.kinds = list(self.kinds)
-        prog.fold_chains = self.fold_chains
+        prog.task_ops = np.asarray(starts + [n], dtype=np.int64)
+        prog.keys = [self.keys[t] for t in order]
+        prog.kinds = [self.kinds[t] for t in order]
+        prog.fold_chains = {u: [newidx[t] for t in ch] for u, ch in self.fold_chains.items()}
         prog.scratch_doubles = max(self.peak, 1)
         prog.scratch_ranks = max(self.rpeak, 1)
         prog.updates = self.updates
-        prog.rw = self.rw
-        prog.peak_task = self.peak_task
+        prog.rw = [self.rw[t] for t in order]
+        prog.peak_task = newidx.get(self.peak_task, -1)
+        prog.groups = {newidx[r]: [newidx[t] for t in ms] for r, ms in self.groups.items()}
+        prog.ws_size = max(self.wtop, 1)
+        prog.ws_slots = max(self.wslots, 1)
         return prog
 
 
@@ -888,11 +984,13 @@ def dataflow_edges(prog, tables):
     return edges
 
 
-def plan_hlu(table: BlockTable, mode: str, policy, rank_cap=None):
-    """Program of H-LU of a matrix over ``table``: A=0, L=1, U=2 (acc=3)."""
+def plan_hlu(table: BlockTable, mode: str, policy, rank_cap=None, split_min=0):
+    """Program of H-LU of a matrix over ``table``: A=0, L=1, U=2 (acc=3,
+    workspace=5).  ``split_min`` > 0 splits H x H products with
+    min(m, n) >= split_min into parallel micro-tasks."""
     lay = Layout(table, rank_cap)
     A, Lm, Um = PMat(0, lay), PMat(1, lay), PMat(2, lay)
-    p = Planner(policy, rank_cap)
+    p = Planner(policy, rank_cap, split_min)
     if mode == "std":
         p.hlu(A, Lm, Um, 0)
     else:

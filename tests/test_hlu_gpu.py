@@ -34,7 +34,7 @@ def product_structure(name):
     return cfg, broot, perm
 
 
-def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64):
+def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256):
     from paper_1911_07531_b200 import hmatrix as H
     from paper_1911_07531_b200.accumulator import AccumulatorMap, hlu_accu
     from paper_1911_07531_b200.arith import hlu
@@ -45,18 +45,19 @@ def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64):
     L, U = H.zeros(broot, pol, rank_cap), H.zeros(broot, pol, rank_cap)
     H.counters.reset()
     if mode == "std":
-        plan = hlu(A, L, U, pol, exec_mode=exec_mode)
+        plan = hlu(A, L, U, pol, exec_mode=exec_mode, split_min=split_min)
     else:
-        plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode)
+        plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode, split_min=split_min)
     return L.store.download_leaves(), U.store.download_leaves(), H.counters.snapshot(), plan
 
 
-@pytest.mark.parametrize("name", ["s1", "s2"])
+@pytest.mark.parametrize("name,split", [("s1", 256), ("s2", 256), ("s2", 32), ("s5", 64)])
 @pytest.mark.parametrize("mode", ["std", "accu"])
-def test_hlu_matches_oracle(name, mode):
+def test_hlu_matches_oracle(name, mode, split):
+    """split: micro-task threshold (32/64 exercise split H x H products)."""
     A, pol, eps = oracle_A(name)
     Lr, Ur, tr, up = O.factor(A, mode, pol)
-    Ld, Ud, (dtr, dup), plan = run_device(name, mode, A.lv)
+    Ld, Ud, (dtr, dup), plan = run_device(name, mode, A.lv, split_min=split)
     bt = A.bt
     Lh, Uh = O.HM(bt, Ld), O.HM(bt, Ud)
     rL, _ = O.leaf_arrays(Lh)
@@ -78,11 +79,12 @@ def test_hlu_matches_oracle(name, mode):
 
 @pytest.mark.parametrize("mode", ["std", "accu"])
 def test_executors_bitwise_identical(mode):
-    """wave / graph / persistent / sequential executions give identical bits."""
+    """wave / graph / persistent / sequential executions give identical bits
+    (with split micro-tasks)."""
     A, pol, eps = oracle_A("s2")
     outs = []
     for em in (3, 0, 1, 2):
-        Ld, Ud, _, _ = run_device("s2", mode, A.lv, exec_mode=em)
+        Ld, Ud, _, _ = run_device("s2", mode, A.lv, exec_mode=em, split_min=32)
         outs.append((Ld, Ud))
     for Ld, Ud in outs[1:]:
         for u, x in outs[0][0].items():
