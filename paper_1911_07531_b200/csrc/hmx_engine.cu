@@ -47,7 +47,7 @@ enum OpCode : int32_t {
 enum : int32_t { F_TA = 1, F_TB = 2, F_ACC = 4 };
 
 constexpr int kScratchBase = 15;
-constexpr int kSmemDoubles = 26624;  // 208 KB dynamic shared memory, 1 CTA per SM
+constexpr int kSmemDoubles = 20480;  // 160 KB dynamic shared memory (leaves ~68 KB of L1), 1 CTA per SM
 constexpr int kSmemWork = kSmemDoubles - 32;
 
 struct DevPlan {
@@ -252,7 +252,7 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   const int p = min(m, K), q = min(n, K);
   // stage U, V (and G) in shared memory when they fit
   const int64_t need = (int64_t)(m + n) * K + 2 * K + (int64_t)p * q;
-  const bool stage = need + 2048 <= kSmemWork;
+  const bool stage = need <= kSmemWork;
   double* G;
   double* smw;
   int smcap;

@@ -19,7 +19,8 @@ mode = mode or cfg.mode
 geom, root, perm, broot = configs.structure(cfg)
 pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
 A0 = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
-plan = get_plan(A0.table, mode, pol, 64)
+split = int(os.environ.get("HMX_SPLIT", "256"))
+plan = get_plan(A0.table, mode, pol, 64, split_min=split)
 A = A0.copy(); L = H.zeros(broot, pol, 64); U = H.zeros(broot, pol, 64)
 plan.run(A.store, L.store, U.store, exe)
 A.store.copy_from(A0.store)
