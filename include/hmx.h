@@ -150,8 +150,9 @@ hmx_status hmx_plan_counters(hmx_plan_t plan, void* stream, uint64_t out[4]);
 hmx_status hmx_plan_reset_counters(hmx_plan_t plan, void* stream);
 /* Per-task timeline: enable != 0 allocates a trace buffer that the
  * executors fill with (start ns, end ns, smid | cta<<32) per task, followed
- * by 16 (busy ns, count) pairs per op code; with out != NULL the last trace
- * is copied to the host (3*n_tasks + 32 words). */
+ * by 16 (busy ns, count) pairs per op code and one duration word per op;
+ * with out != NULL the last trace is copied to the host
+ * (3*n_tasks + 32 + n_ops words). */
 hmx_status hmx_plan_trace(hmx_plan_t plan, int32_t enable, uint64_t* out);
 hmx_status hmx_plan_destroy(hmx_plan_t plan);
 

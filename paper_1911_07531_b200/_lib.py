@@ -153,6 +153,7 @@ class Plan:
         self.h = h
         self._keep = None
         self.n_tasks = len(to) - 1
+        self.n_ops = len(o)
 
     def bind(self, base_id, values, ranks=None):
         check(lib().hmx_plan_bind(self.h, int(base_id), ptr(values), ptr(ranks)), "plan_bind")
@@ -177,10 +178,11 @@ class Plan:
         check(lib().hmx_plan_trace(self.h, int(bool(on)), None), "plan_trace")
 
     def trace(self):
-        out = np.zeros(3 * self.n_tasks + 32, dtype=np.uint64)
+        out = np.zeros(3 * self.n_tasks + 32 + self.n_ops, dtype=np.uint64)
         check(lib().hmx_plan_trace(self.h, 1, out.ctypes.data_as(C.c_void_p)), "plan_trace")
         t = out[:3 * self.n_tasks].reshape(-1, 3)
-        self.op_profile = out[3 * self.n_tasks:].reshape(16, 2).astype(np.int64)
+        self.op_profile = out[3 * self.n_tasks:3 * self.n_tasks + 32].reshape(16, 2).astype(np.int64)
+        self.op_times = out[3 * self.n_tasks + 32:].astype(np.int64)
         return t[:, 0].astype(np.int64), t[:, 1].astype(np.int64), (t[:, 2] & 0xffffffff).astype(np.int64)
 
     def close(self):

@@ -30,6 +30,13 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+template <int G>
+__device__ __forceinline__ double seg_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // Block-wide sum; `red` is HMX_WARPS doubles of shared memory.  All threads
 // receive the result.
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -273,56 +280,97 @@ __device__ __forceinline__ void warp_apply_reflector(int m, int j, const double*
   for (int i = i0; i < m; i += 32) y[i] -= d * (i == j ? 1.0 : v[i]);
 }
 
-__device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau, double* red) {
-  const int p = min(m, K);
-  const int w = threadIdx.x >> 5;
-  for (int j = 0; j < p; ++j) {
-    double* x = A + (int64_t)j * lda;
-    if (w == 0) warp_reflector(m, j, x, tau);
-    __syncthreads();
-    const double t = tau[j];
-    if (t != 0.0)
-      for (int c = j + 1 + w; c < K; c += HMX_WARPS)
-        warp_apply_reflector(m, j, x, t, A + (int64_t)c * lda);
-    __syncthreads();
-  }
-}
-
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// y := H_j y by a group of G lanes (G divides 32); lane gl owns the rows
+// i = gl (mod G).  Several columns are processed concurrently by the groups
+// of a warp, so each reduction is log2(G) shuffle levels deep instead of 5.
+// All 32 lanes of a warp must call this (the shuffles are warp-wide).
+template <int G>
+__device__ __forceinline__ void grp_apply_reflector(int m, int j, const double* v, double t,
+                                                    double* y, int gl, bool active) {
+  double d = 0.0;
+  const int i0 = j + ((gl - j) & (G - 1));
+  if (active)
+    for (int i = i0; i < m; i += G) d = fma(i == j ? 1.0 : v[i], y[i], d);
+  d = seg_sum<G>(d) * t;
+  if (active)
+    for (int i = i0; i < m; i += G) y[i] -= d * (i == j ? 1.0 : v[i]);
+}
+
+// Apply reflector j (column x) to columns [c0, K) of A with `nthreads`
+// threads starting at thread t0 (whole warps).
+template <int G>
+__device__ __forceinline__ void grp_update_cols(int m, int j, const double* x, double t, double* A,
+                                                int lda, int c0, int K, int t0, int nthreads) {
+  const int tid = (int)threadIdx.x - t0;
+  const int grp = tid / G, gl = tid % G, ngrp = nthreads / G;
+  const int njobs = K - c0;
+  for (int b = 0; b < njobs; b += ngrp) {
+    const int c = c0 + b + grp;
+    grp_apply_reflector<G>(m, j, x, t, A + (int64_t)min(c, K - 1) * lda, gl, c < K);
+  }
+}
+
+template <int G>
+__device__ void qr_steps(int m, int K, double* A, int lda, double* tau, int wbeg, int nw, int bar) {
+  const int p = min(m, K);
+  const int w = (int)(threadIdx.x >> 5) - wbeg;
+  for (int j = 0; j < p; ++j) {
+    double* x = A + (int64_t)j * lda;
+    if (w == 0) warp_reflector(m, j, x, tau);
+    if (bar) named_bar(bar, nw * 32); else __syncthreads();
+    const double t = tau[j];
+    if (t != 0.0) grp_update_cols<G>(m, j, x, t, A, lda, j + 1, K, wbeg * 32, nw * 32);
+    if (bar) named_bar(bar, nw * 32); else __syncthreads();
+  }
+}
+
+
+// G (lanes per column) from the row count: ~8 rows per lane.
+#define HMX_G_DISPATCH(m, CALL)            \
+  do {                                     \
+    if ((m) <= 64) { constexpr int GG = 8; CALL; }        \
+    else if ((m) <= 128) { constexpr int GG = 16; CALL; } \
+    else { constexpr int GG = 32; CALL; }                 \
+  } while (0)
+
+__device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau, double* red) {
+  HMX_G_DISPATCH(m, (qr_steps<GG>(m, K, A, lda, tau, 0, HMX_WARPS, 0)));
+}
+
 
 // Householder QR by a group of nw warps [wbeg, wbeg + nw) synchronised on
 // named barrier bar_id, so that two factorizations (U and V of a
 // truncation) run concurrently in one CTA.
 __device__ void group_householder_qr(int m, int K, double* A, int lda, double* tau, int wbeg,
                                      int nw, int bar_id) {
-  const int p = min(m, K);
-  const int w = (int)(threadIdx.x >> 5) - wbeg;
-  for (int j = 0; j < p; ++j) {
-    double* x = A + (int64_t)j * lda;
-    if (w == 0) warp_reflector(m, j, x, tau);
-    named_bar(bar_id, nw * 32);
-    const double t = tau[j];
-    if (t != 0.0)
-      for (int c = j + 1 + w; c < K; c += nw)
-        warp_apply_reflector(m, j, x, t, A + (int64_t)c * lda);
-    named_bar(bar_id, nw * 32);
-  }
+  HMX_G_DISPATCH(m, (qr_steps<GG>(m, K, A, lda, tau, wbeg, nw, bar_id)));
 }
 
 // X (m x r) := Q X where Q = H_0 H_1 ... H_{p-1} from cta_householder_qr.
-// Columns of X are independent: one warp per column, no block barriers.
-__device__ void cta_apply_q(int m, int p, const double* A, int lda, const double* tau, int r,
-                            double* X, int ldx) {
-  const int w = threadIdx.x >> 5;
-  for (int c = w; c < r; c += HMX_WARPS) {
-    double* y = X + (int64_t)c * ldx;
+// Columns of X are independent: one lane group per column, no block
+// barriers between reflectors.
+template <int G>
+__device__ void apply_q_cols(int m, int p, const double* A, int lda, const double* tau, int r,
+                             double* X, int ldx) {
+  const int grp = threadIdx.x / G, gl = threadIdx.x % G, ngrp = HMX_THREADS / G;
+  for (int b = 0; b < r; b += ngrp) {
+    const int c = b + grp;
+    const bool act = c < r;
+    double* y = X + (int64_t)min(c, max(r - 1, 0)) * ldx;
     for (int j = p - 1; j >= 0; --j) {
       const double t = tau[j];
-      if (t != 0.0) warp_apply_reflector(m, j, A + (int64_t)j * lda, t, y);
+      if (t != 0.0) grp_apply_reflector<G>(m, j, A + (int64_t)j * lda, t, y, gl, act);
     }
   }
+}
+
+__device__ void cta_apply_q(int m, int p, const double* A, int lda, const double* tau, int r,
+                            double* X, int ldx) {
+  if (r > 0) HMX_G_DISPATCH(m, (apply_q_cols<GG>(m, p, A, lda, tau, r, X, ldx)));
   __syncthreads();
 }
 
@@ -338,12 +386,6 @@ __device__ void cta_apply_q(int m, int p, const double* A, int lda, const double
 // One-sided Jacobi has high relative accuracy, so singular values near the
 // eps*sigma_1 cut agree with LAPACK's dgesdd (hmatrix.py:126) to rounding.
 // ---------------------------------------------------------------------------
-template <int G>
-__device__ __forceinline__ double seg_sum(double v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 template <int G>
 __device__ void jacobi_rounds(int p, int q, double* Gm, int ldg, double* J, int ldj, double tol2,
@@ -370,11 +412,12 @@ __device__ void jacobi_rounds(int p, int q, double* Gm, int ldg, double* J, int 
       double al = 0.0, be = 0.0, ga = 0.0;
       double* x = Gm + (int64_t)a * ldg;
       double* y = Gm + (int64_t)b * ldg;
-      if (valid)
+      if (valid) {
         for (int i = gl; i < p; i += G) {
           const double u = x[i], v = y[i];
           al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
         }
+      }
       al = seg_sum<G>(al); be = seg_sum<G>(be); ga = seg_sum<G>(ga);
       if (!valid || al == 0.0 || be == 0.0 || ga * ga <= tol2 * al * be) continue;
       const double zeta = (be - al) / (2.0 * ga);
@@ -554,15 +597,15 @@ __device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm
     __syncthreads();
     const double t = tau[j];
     const double* x = G + (int64_t)j * ldg;
+    if (t != 0.0) HMX_G_DISPATCH(p, (grp_update_cols<GG>(p, j, x, t, G, ldg, j + 1, q, 0, HMX_THREADS)));
+    __syncthreads();
+    // norm downdate (dlaqp2): one warp per column; recompute on cancellation
     for (int c = j + 1 + w; c < q; c += HMX_WARPS) {
-      double* y = G + (int64_t)c * ldg;
-      if (t != 0.0) warp_apply_reflector(p, j, x, t, y);
-      __syncwarp();
+      const double* y = G + (int64_t)c * ldg;
       const double rj = y[j];
       const double nv = cn[c] - rj * rj;
       const bool rec = !(nv > 1e-4 * cn0[c]);
-      __syncwarp();
-      if (rec) {  // dlaqp2: recompute after severe cancellation
+      if (rec) {
         double s2 = 0.0;
         for (int i = j + 1 + lane; i < p; i += 32) s2 = fma(y[i], y[i], s2);
         s2 = warp_sum(s2);

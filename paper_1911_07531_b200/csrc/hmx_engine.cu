@@ -213,6 +213,46 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   return r;
 }
 
+// Each lane group works on a private shared-memory copy of its output
+// column (lane gl owns rows i = gl mod G for the copy-in, every reflector
+// and the copy-out), so the reflector chain never round-trips through L2.
+template <int G>
+__device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const double* Gq, int ldgq,
+                               const double* tau_g, const double* U, int ldu, const double* tau_u,
+                               const double* V, int ldv, const double* tau_v, double* Uo, int lduo,
+                               double* Vo, int ldvo, double* colbuf) {
+  const int grp = threadIdx.x / G, gl = threadIdx.x % G, ngrp = HMX_THREADS / G;
+  double* y = colbuf + (int64_t)grp * max(m, n);
+  // U jobs and V jobs are issued in separate passes so that the reflector
+  // loops of one pass have uniform trip counts across a warp
+  for (int b = 0; b < r; b += ngrp) {
+    const int c = b + grp;
+    const bool act = c < r;
+    double* yo = Uo + (int64_t)min(c, r - 1) * lduo;
+    if (act) for (int i = gl; i < m; i += G) y[i] = yo[i];
+    for (int j = kg - 1; j >= 0; --j) {
+      const double t = tau_g[j];
+      if (t != 0.0) grp_apply_reflector<G>(p, j, Gq + (int64_t)j * ldgq, t, y, gl, act);
+    }
+    for (int j = p - 1; j >= 0; --j) {
+      const double t = tau_u[j];
+      if (t != 0.0) grp_apply_reflector<G>(m, j, U + (int64_t)j * ldu, t, y, gl, act);
+    }
+    if (act) for (int i = gl; i < m; i += G) yo[i] = y[i];
+  }
+  for (int b = 0; b < r; b += ngrp) {
+    const int c = b + grp;
+    const bool act = c < r;
+    double* yo = Vo + (int64_t)min(c, r - 1) * ldvo;
+    if (act) for (int i = gl; i < n; i += G) y[i] = yo[i];
+    for (int j = q - 1; j >= 0; --j) {
+      const double t = tau_v[j];
+      if (t != 0.0) grp_apply_reflector<G>(n, j, V + (int64_t)j * ldv, t, y, gl, act);
+    }
+    if (act) for (int i = gl; i < n; i += G) yo[i] = y[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // truncate (hmatrix.py:113-130): QR(U), QR(V), SVD(Ru Rv^T), keep, recompose
 // ---------------------------------------------------------------------------
@@ -252,7 +292,9 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   const int p = min(m, K), q = min(n, K);
   // stage U, V (and G) in shared memory when they fit
   const int64_t need = (int64_t)(m + n) * K + 2 * K + (int64_t)p * q;
-  const bool stage = need <= kSmemWork;
+  const int Lmn = max(m, n);
+  const int colneed = (Lmn <= 64 ? 32 : (Lmn <= 128 ? 16 : 8)) * Lmn;  // recomposition buffers
+  const bool stage = need + colneed <= kSmemWork;
   double* G;
   double* smw;
   int smcap;
@@ -310,27 +352,11 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   __syncthreads();
   if (stage) {
     // fused recomposition: U columns get Q_G then Q_u, V columns Q_v; one
-    // warp per column job, no block barriers between reflectors
-    const int w = threadIdx.x >> 5;
-    for (int job = w; job < 2 * r; job += HMX_WARPS) {
-      if (job < r) {
-        double* y = Uo + (int64_t)job * lduo;
-        for (int j = kg - 1; j >= 0; --j) {
-          const double t = tau_g[j];
-          if (t != 0.0) warp_apply_reflector(p, j, Gq + (int64_t)j * ldgq, t, y);
-        }
-        for (int j = p - 1; j >= 0; --j) {
-          const double t = tau_u[j];
-          if (t != 0.0) warp_apply_reflector(m, j, U + (int64_t)j * ldu_q, t, y);
-        }
-      } else {
-        double* y = Vo + (int64_t)(job - r) * ldvo;
-        for (int j = q - 1; j >= 0; --j) {
-          const double t = tau_v[j];
-          if (t != 0.0) warp_apply_reflector(n, j, V + (int64_t)j * ldv_q, t, y);
-        }
-      }
-    }
+    // lane group per column job, no block barriers between reflectors
+    // column buffers after G (X/J are dead by now): colneed doubles
+    double* colbuf = Gq + (int64_t)p * q;
+    HMX_G_DISPATCH(max(m, n), (recompose_jobs<GG>(r, p, q, m, n, kg, Gq, ldgq, tau_g, U, ldu_q, tau_u,
+                                                   V, ldv_q, tau_v, Uo, lduo, Vo, ldvo, colbuf)));
     __syncthreads();
   } else {
     cta_apply_q_blocked(m, p, Vxu, m, Tu, r, Uo, lduo, Wq, work, kSmemWork);
@@ -359,7 +385,7 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* work = sm + 32;
   double* G = M;
   int ldg = ldm;
-  const bool gsm = m * n <= kSmemWork / 2 + kSmemWork / 4;
+  const bool gsm = m * n + 64 <= kSmemWork;
   if (gsm) {
     G = work;
     ldg = m;
@@ -535,10 +561,13 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
     if (P.trace && threadIdx.x == 0) q0 = gtimer();
     run_op(P, c, o, sm);
     if (P.trace && threadIdx.x == 0) {
-      // per-opcode busy time and count, after the task records (3*n_tasks words)
+      // per-opcode busy time and count, after the task records (3*n_tasks
+      // words), then one duration word per op
       unsigned long long* prof = P.trace + 3 * (int64_t)P.n_tasks;
-      atomicAdd(&prof[2 * (o.code & 15)], gtimer() - q0);
+      const unsigned long long dt = gtimer() - q0;
+      atomicAdd(&prof[2 * (o.code & 15)], dt);
       atomicAdd(&prof[2 * (o.code & 15) + 1], 1ull);
+      prof[32 + i] = dt;
     }
   }
   if (threadIdx.x == 0) {
@@ -901,7 +930,8 @@ hmx_status hmx_plan_trace(hmx_plan_t p, int32_t enable, uint64_t* out) {
   if (!p) return HMX_ERR_ARG;
   cudaError_t e = cudaSuccess;
   if (enable && !p->d_trace) {
-    e = cudaMalloc(&p->d_trace, (3 * (size_t)std::max(p->n_tasks, 1) + 32) * sizeof(unsigned long long));
+    e = cudaMalloc(&p->d_trace, (3 * (size_t)std::max(p->n_tasks, 1) + 32 + (size_t)p->n_ops) *
+                                    sizeof(unsigned long long));
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
   } else if (!enable && p->d_trace && !out) {
     e = cudaFree(p->d_trace);
@@ -909,7 +939,8 @@ hmx_status hmx_plan_trace(hmx_plan_t p, int32_t enable, uint64_t* out) {
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
   }
   if (!e && out && p->d_trace)
-    e = cudaMemcpy(out, p->d_trace, (3 * (size_t)p->n_tasks + 32) * sizeof(unsigned long long),
+    e = cudaMemcpy(out, p->d_trace, (3 * (size_t)p->n_tasks + 32 + (size_t)p->n_ops) *
+                                        sizeof(unsigned long long),
                    cudaMemcpyDeviceToHost);
   return cuda_status(e);
 }

@@ -82,6 +82,22 @@ for t in path:
     for o in ops[plan.prog.task_ops[t]:plan.prog.task_ops[t + 1]]:
         oc[int(o["code"])] += 1
 print("  ops on path", dict(oc))
+# exact per-op time on the critical path (per-op device durations)
+opt = plan.plan.op_times
+pc, pn = Counter(), Counter()
+for t in path:
+    a, b = plan.prog.task_ops[t], plan.prog.task_ops[t + 1]
+    for i in range(a, b):
+        code = int(ops[i]["code"])
+        key = names.get(code, code)
+        if code == 8:
+            K = int(ops[i]["dim"][0])
+            key = f"TRUNC m={K}"
+        pc[key] += opt[i] / 1e3
+        pn[key] += 1
+print("  critical-path time by op:")
+for k, v in pc.most_common(14):
+    print(f"    {k:16s} {v/1e3:8.2f} ms  n={pn[k]}")
 pd = sorted(path, key=lambda t: -dur[t])[:25]
 for t in pd:
     o = ops[plan.prog.task_ops[t]:plan.prog.task_ops[t + 1]]
