@@ -115,3 +115,47 @@ def test_reference_fixture_ranks(name):
         got = O.apply(O.HM(bt, Ld), 0, O.apply(O.HM(bt, Ud), 0, X))
         want = arr[f"{mode}_probe_LUx"]
         assert np.linalg.norm(got - want) <= 10 * eps * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("mode", ["accu", "std"])
+def test_c2_ranks_bit_exact_vs_reference(mode):
+    """BASELINE config 2 end to end on the device: assembly ranks, every
+    L/U block rank and the truncation/update counters equal the unmodified
+    reference's run (tests/golden/c2.*); probe products within 10*eps."""
+    if not have("c2"):
+        pytest.skip("fixture missing")
+    from paper_1911_07531_b200 import configs, hmatrix as H
+    from paper_1911_07531_b200.accumulator import AccumulatorMap, hlu_accu
+    from paper_1911_07531_b200.arith import hlu
+
+    meta, arr = load("c2")
+    cfg = configs.config("c2")
+    geom, root, perm, broot = configs.structure(cfg)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    rA = A.store.ranks.cpu().numpy()
+    sel = arr["A_rank"] >= 0
+    assert np.array_equal(rA[sel], arr["A_rank"][sel])
+    L, U = H.zeros(broot, pol, 64), H.zeros(broot, pol, 64)
+    H.counters.reset()
+    if mode == "std":
+        hlu(A, L, U, pol)
+    else:
+        hlu_accu(A, L, U, AccumulatorMap(), pol)
+    tr, up = H.counters.snapshot()
+    assert tr == meta[f"{mode}_truncations"]
+    assert up == meta[f"{mode}_updates"]
+    rl = L.store.ranks.cpu().numpy()
+    ru = U.store.ranks.cpu().numpy()
+    sel = arr[f"{mode}_L_rank"] >= 0
+    assert np.array_equal(rl[sel], arr[f"{mode}_L_rank"][sel]), int((rl[sel] != arr[f"{mode}_L_rank"][sel]).sum())
+    assert np.array_equal(ru[sel], arr[f"{mode}_U_rank"][sel]), int((ru[sel] != arr[f"{mode}_U_rank"][sel]).sum())
+    bt = O.BlockTable(0)
+    # probe through the oracle's apply on the downloaded factors
+    ct = O.cluster_tree(cfg.points, cfg.n_min)
+    bt = O.block_tree(ct, O.adm_standard(ct, cfg.eta))
+    Lh, Uh = O.HM(bt, L.store.download_leaves()), O.HM(bt, U.store.download_leaves())
+    X = arr["probe_x"]
+    got = O.apply(Lh, 0, O.apply(Uh, 0, X))
+    want = arr[f"{mode}_probe_LUx"]
+    assert np.linalg.norm(got - want) <= 10 * cfg.eps * np.linalg.norm(want)

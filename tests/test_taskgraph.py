@@ -105,3 +105,29 @@ def test_levels_and_csr():
     for i in range(g.n_nodes):
         for j in idx[ptr[i]:ptr[i + 1]]:
             assert lv[j] > lv[i]
+
+
+@pytest.mark.parametrize("name", ["c3s", "c5s"])
+def test_large_trees_match_reference(name):
+    """Configs 3 and 5: cluster tree, permutation and block tree bit-exact."""
+    if not have(name):
+        pytest.skip("fixture missing")
+    meta, _ = load(name)
+    cfg = configs.config(name[:2])
+    geom, root, perm, broot = configs.structure(cfg)
+    assert _sha(serialize_cluster_tree(root)) == meta["cluster_sha"]
+    assert _sha(",".join(map(str, perm.tolist()))) == meta["perm_sha"]
+    assert _sha(serialize_block_tree(broot)) == meta["block_sha"]
+
+
+@pytest.mark.slow
+def test_c3_dags_match_reference():
+    meta, _ = load("c3s")
+    cfg = configs.config("c3")
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    for tag, mode in (("std", "std"), ("accu-merged", "accu-merged")):
+        g = tg.build_hlu_dag(bt, mode)
+        ref = meta["dags"][tag]
+        assert g.stats() == (ref["nodes"], ref["edges"])
+        assert tg.canonical_hashes(g) == (ref["nodes_sha"], ref["edges_sha"])
