@@ -85,3 +85,52 @@ def dense_lu(A: np.ndarray):
     if info[0]:
         raise SingularPivotError("vanishing pivot")
     return Ls[0], Us[0]
+
+
+_OPS = {}
+
+
+def _op_plan(table, op, policy, rank_cap, alpha=1.0):
+    key = (id(table), op, repr(policy), rank_cap, float(alpha))
+    p = _OPS.get(key)
+    if p is None or p.table is not table:
+        p = engine.OpPlan(table, op, policy, rank_cap, alpha=alpha)
+        _OPS[key] = p
+    return p
+
+
+def _run_op(op, M0, M1, M2, policy, alpha=1.0, **kw):
+    t = _check_operands(M0, M1, M2)
+    rc = M0.store.layout.rank_cap
+    if any(M.store.layout.rank_cap != rc for M in (M1, M2)):
+        raise ValueError("operand storage rank_cap differs")
+    if M2.store is M0.store or M2.store is M1.store:
+        raise ValueError("the output may not alias an input")
+    plan = _op_plan(t, op, policy, rc, alpha)
+    plan.run(M0.store, M1.store, M2.store, **kw)
+    c = plan.counters()
+    counters.add(c["truncations"], c["updates"])
+    return plan
+
+
+def hmul(alpha: float, A: HMatrix, B: HMatrix, C: HMatrix, policy: TruncationPolicy, **kw):
+    """C += alpha * A @ B over matching block structures (arith.py:40-55)."""
+    if alpha == 0.0:
+        return None
+    if A.nrows != C.nrows or B.ncols != C.ncols or A.ncols != B.nrows:
+        raise ValueError("non-conformal hmul operands")
+    return _run_op("hmul", A, B, C, policy, alpha=alpha, **kw)
+
+
+def htrsl(L: HMatrix, M: HMatrix, X: HMatrix, policy: TruncationPolicy, **kw):
+    """Solve L X = M (L unit lower triangular); M is consumed (arith.py:97-117)."""
+    if L.nrows != M.nrows or M.nrows != L.ncols:
+        raise ValueError("non-conformal triangular solve")
+    return _run_op("htrsl", L, M, X, policy, **kw)
+
+
+def htrsu(U: HMatrix, M: HMatrix, X: HMatrix, policy: TruncationPolicy, **kw):
+    """Solve X U = M (U upper triangular); M is consumed (arith.py:120-140)."""
+    if U.ncols != M.ncols or M.ncols != U.nrows:
+        raise ValueError("non-conformal triangular solve")
+    return _run_op("htrsu", U, M, X, policy, **kw)

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _lib
 from . import taskgraph as tg
-from .planner import ACC_BASE_ID, Layout, dataflow_edges, plan_hlu
+from .planner import ACC_BASE_ID, Layout, dataflow_edges, plan_hlu, plan_op
 from .trees import BlockTable
 
 EXEC_WAVE, EXEC_GRAPH, EXEC_PERSISTENT, EXEC_SEQUENTIAL = 0, 1, 2, 3
@@ -312,3 +312,59 @@ class ExecPlan:
                 "max_wave": int(w.max()) if len(w) else 0,
                 "scratch_mb_per_cta": self.prog.scratch_doubles * 8 / 2**20,
                 "acc_mb": self.prog.acc_size * 8 / 2**20, "pool_mb": self.layout.size * 8 / 2**20}
+
+
+class OpPlan:
+    """Standalone multiply / triangular-solve plan (hmul, htrsl, htrsu and
+    the accumulator solves).  Tasks are the leaf-level calls of the
+    reference recursion (the final nodes of the refined multiply / TRSM
+    DAGs, taskgraph.py:146-180); the execution graph comes from the data
+    flow of the sequential recursion."""
+
+    def __init__(self, table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, max_ctas=0):
+        self.table = table
+        self.op = op
+        prog = plan_op(table, op, policy, rank_cap, alpha=alpha)
+        self.prog = prog
+        self.layout = prog.layout
+        tables = {b: table for b in range(4)}
+        edges = dataflow_edges(prog, tables)
+        n = len(prog.keys)
+        src = np.fromiter((a for a, _ in edges), dtype=np.int64, count=len(edges))
+        dst = np.fromiter((b for _, b in edges), dtype=np.int64, count=len(edges))
+        o = np.lexsort((dst, src))
+        src, dst = src[o], dst[o]
+        ptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(ptr, src + 1, 1)
+        ptr = np.cumsum(ptr).astype(np.int32)
+        idx = dst.astype(np.int32)
+        lv = tg.asap_levels(n, ptr, idx) if n else np.zeros(0, np.int32)
+        order = np.argsort(lv, kind="stable").astype(np.int32)
+        counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
+        wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+        self.n_tasks = n
+        self.plan = _lib.Plan(prog.ops, prog.task_ops, ptr, idx, wave_ptr, order,
+                              prog.scratch_doubles, prog.scratch_ranks, max_ctas)
+        torch = _torch()
+        self.acc_values = torch.zeros(prog.acc_size, dtype=torch.float64, device="cuda")
+        self.acc_ranks = torch.zeros(max(table.n, 1), dtype=torch.int32, device="cuda")
+        self.plan.bind(ACC_BASE_ID, self.acc_values, self.acc_ranks)
+        self.ws_values = torch.zeros(getattr(prog, "ws_size", 1), dtype=torch.float64, device="cuda")
+        self.ws_ranks = torch.zeros(getattr(prog, "ws_slots", 1), dtype=torch.int32, device="cuda")
+        self.plan.bind(WS_BASE_ID, self.ws_values, self.ws_ranks)
+
+    def run(self, s0: HStore, s1: HStore, s2: HStore, exec_mode=EXEC_PERSISTENT, stream=None):
+        for i, st in enumerate((s0, s1, s2)):
+            if st.layout.table is not self.table:
+                raise ValueError("operand is not over the plan's block tree")
+            self.plan.bind(i, st.values, st.ranks)
+        self.plan.reset_counters(stream)
+        self.plan.execute(exec_mode, stream)
+        stt = self.plan.status(stream)
+        if stt:
+            raise _lib.HmxError(stt, self.op)
+
+    def counters(self, stream=None):
+        c = self.plan.counters(stream)
+        return {"truncations": c[0], "flops": c[1], "bytes": c[2], "tasks": c[3],
+                "updates": self.prog.updates}

@@ -1043,3 +1043,36 @@ def replicate(prog, nrep, base_sizes, slot_sizes):
     t_all = (task_ops[None, :-1] + (np.arange(nrep)[:, None] * n)).ravel()
     new_task_ops = np.concatenate([t_all, [n * nrep]]).astype(np.int64)
     return out, new_task_ops, nt
+
+
+OPS = ("hmul", "htrsl", "htrsu", "htrsl_accu", "htrsu_accu")
+
+
+def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_min=0):
+    """Program of a standalone multiply / triangular solve over ``table``.
+
+    hmul:  C += alpha A B          (arith.py:40-55)      A=0, B=1, C=2
+    htrsl: L X = M, M consumed     (arith.py:97-117)     L=0, M=1, X=2
+    htrsu: X U = M, M consumed     (arith.py:120-140)    U=0, M=1, X=2
+    *_accu: the accumulator variants (accumulator.py:190-235), acc=3
+    """
+    if op not in OPS:
+        raise ValueError(op)
+    lay = Layout(table, rank_cap)
+    P0, P1, P2 = PMat(0, lay), PMat(1, lay), PMat(2, lay)
+    p = Planner(policy, rank_cap, split_min)
+    if op == "hmul":
+        p.hmul(alpha, P0, 0, P1, 0, P2, 0)
+    elif op == "htrsl":
+        p.htrsl(P0, 0, P1, 0, P2)
+    elif op == "htrsu":
+        p.htrsu(P0, 0, P1, 0, P2)
+    else:
+        p.acc_table = table
+        if op == "htrsl_accu":
+            p.htrsl_accu(P0, 0, P1, 0, P2)
+        else:
+            p.htrsu_accu(P0, 0, P1, 0, P2)
+    prog = p.pack()
+    prog.layout = lay
+    return prog
