@@ -162,7 +162,10 @@ class ExecPlan:
         if (mode == "std") != (dag_mode == tg.STD):
             raise ValueError(f"DAG mode {dag_mode} does not execute {mode} arithmetic")
         if dag_mode == tg.COMBINED:
-            raise NotImplementedError("combined-mode execution: use accu-merged")
+            from .planner import fuse_applies
+
+            prog = fuse_applies(prog)
+            self.prog = prog
         self.dag_mode = dag_mode
         self.dag = tg.build_hlu_dag(table, dag_mode, sparsify=sparsify)
         ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()

@@ -1076,3 +1076,51 @@ def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_
     prog = p.pack()
     prog.layout = lay
     return prog
+
+
+def fuse_applies(prog):
+    """Combined accumulator mode: fold every apply_upd task into the leaf
+    factor/solve task that follows it in program order (the combined DAG has
+    no apply nodes; its leaf tasks apply first)."""
+    keys, kinds = prog.keys, prog.kinds
+    n = len(keys)
+    keep = []
+    merged_into = {}
+    i = 0
+    while i < n:
+        if kinds[i] == "apply_upd":
+            j = i + 1
+            if j >= n or kinds[j] not in ("leaf_factor", "leaf_solve_l", "leaf_solve_u") \
+                    or keys[j][1][-1] != keys[i][1][0]:
+                raise RuntimeError("apply_upd not followed by its leaf task")
+            merged_into[i] = len(keep)
+            merged_into[j] = len(keep)
+            keep.append((i, j))
+            i += 2
+        else:
+            merged_into[i] = len(keep)
+            keep.append((i,))
+            i += 1
+    ops_parts, starts, nkeys, nkinds, nrw = [], [], [], [], []
+    cur = 0
+    for grp in keep:
+        starts.append(cur)
+        for t in grp:
+            a, b = prog.task_ops[t], prog.task_ops[t + 1]
+            ops_parts.append(prog.ops[a:b])
+            cur += b - a
+        last = grp[-1]
+        nkeys.append(keys[last])
+        nkinds.append(kinds[last])
+        r, w = [], []
+        for t in grp:
+            r.extend(prog.rw[t][0])
+            w.extend(prog.rw[t][1])
+        nrw.append((r, w))
+    prog.ops = np.concatenate(ops_parts) if ops_parts else prog.ops[:0]
+    prog.task_ops = np.asarray(starts + [cur], dtype=np.int64)
+    prog.keys, prog.kinds, prog.rw = nkeys, nkinds, nrw
+    prog.fold_chains = {u: [merged_into[t] for t in ch] for u, ch in prog.fold_chains.items()}
+    prog.groups = {merged_into[r]: [merged_into[t] for t in ms] for r, ms in prog.groups.items()}
+    prog.peak_task = merged_into.get(prog.peak_task, -1)
+    return prog

@@ -34,7 +34,7 @@ def product_structure(name):
     return cfg, broot, perm
 
 
-def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256):
+def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256, dag_mode=None):
     from paper_1911_07531_b200 import hmatrix as H
     from paper_1911_07531_b200.accumulator import AccumulatorMap, hlu_accu
     from paper_1911_07531_b200.arith import hlu
@@ -47,7 +47,8 @@ def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256):
     if mode == "std":
         plan = hlu(A, L, U, pol, exec_mode=exec_mode, split_min=split_min)
     else:
-        plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode, split_min=split_min)
+        plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode, split_min=split_min,
+                        dag_mode=dag_mode)
     return L.store.download_leaves(), U.store.download_leaves(), H.counters.snapshot(), plan
 
 
@@ -75,6 +76,20 @@ def test_hlu_matches_oracle(name, mode, split):
     AX = O.apply(A, 0, X)
     res = np.linalg.norm(AX - got) / np.linalg.norm(AX)
     assert res <= 100 * eps
+
+
+def test_combined_mode_equals_merged():
+    """accu-combined DAG execution (apply fused into leaf tasks) gives the
+    same bits as accu-merged (both replay hlu_accu)."""
+    A, pol, eps = oracle_A("s2")
+    a = run_device("s2", "accu", A.lv, dag_mode="accu-merged")
+    b = run_device("s2", "accu", A.lv, dag_mode="accu-combined")
+    assert b[3].n_tasks == 5241 + 80 or b[3].dag.n_nodes == 5241
+    for x, y in zip(a[:2], b[:2]):
+        for u, v in x.items():
+            for p, q in zip(v[1:], y[u][1:]):
+                assert np.array_equal(p, q)
+    assert a[2] == b[2]
 
 
 @pytest.mark.parametrize("mode", ["std", "accu"])
