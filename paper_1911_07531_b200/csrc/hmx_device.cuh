@@ -284,6 +284,40 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Lanes per column G: minimise (passes over the jobs) x (latency of one
+// reflector application ~ 30 cycles per owned row + 35 per shuffle level +
+// 100 fixed), measured primitive latencies of tools/probes/latency.cu.
+__device__ __forceinline__ int pick_g(int m, int jobs, int nthreads) {
+  int best = 32;
+  long best_cost = 1L << 60;
+#pragma unroll
+  for (int lg = 2; lg <= 5; ++lg) {
+    const int g = 1 << lg;
+    const long passes = (jobs * (long)g + nthreads - 1) / nthreads;
+    const long cost = passes * ((m + g - 1) / g * 30 + lg * 35 + 100);
+    if (cost < best_cost) { best_cost = cost; best = g; }
+  }
+  return best;
+}
+
+#define HMX_G_SWITCH(g, CALL)                                   \
+  do {                                                          \
+    switch (g) {                                                \
+      case 4: { constexpr int GG = 4; CALL; } break;            \
+      case 8: { constexpr int GG = 8; CALL; } break;            \
+      case 16: { constexpr int GG = 16; CALL; } break;          \
+      default: { constexpr int GG = 32; CALL; } break;          \
+    }                                                           \
+  } while (0)
+
+// G from the row count alone (~8 rows per lane), for fixed-structure loops.
+#define HMX_G_DISPATCH(m, CALL)            \
+  do {                                     \
+    if ((m) <= 64) { constexpr int GG = 8; CALL; }        \
+    else if ((m) <= 128) { constexpr int GG = 16; CALL; } \
+    else { constexpr int GG = 32; CALL; }                 \
+  } while (0)
+
 // y := H_j y by a group of G lanes (G divides 32); lane gl owns the rows
 // i = gl (mod G).  Several columns are processed concurrently by the groups
 // of a warp, so each reduction is log2(G) shuffle levels deep instead of 5.
@@ -293,11 +327,15 @@ __device__ __forceinline__ void grp_apply_reflector(int m, int j, const double* 
                                                     double* y, int gl, bool active) {
   double d = 0.0;
   const int i0 = j + ((gl - j) & (G - 1));
-  if (active)
+  if (active) {
+#pragma unroll 4
     for (int i = i0; i < m; i += G) d = fma(i == j ? 1.0 : v[i], y[i], d);
+  }
   d = seg_sum<G>(d) * t;
-  if (active)
+  if (active) {
+#pragma unroll 4
     for (int i = i0; i < m; i += G) y[i] -= d * (i == j ? 1.0 : v[i]);
+  }
 }
 
 // Apply reflector j (column x) to columns [c0, K) of A with `nthreads`
@@ -314,7 +352,6 @@ __device__ __forceinline__ void grp_update_cols(int m, int j, const double* x, d
   }
 }
 
-template <int G>
 __device__ void qr_steps(int m, int K, double* A, int lda, double* tau, int wbeg, int nw, int bar) {
   const int p = min(m, K);
   const int w = (int)(threadIdx.x >> 5) - wbeg;
@@ -323,22 +360,15 @@ __device__ void qr_steps(int m, int K, double* A, int lda, double* tau, int wbeg
     if (w == 0) warp_reflector(m, j, x, tau);
     if (bar) named_bar(bar, nw * 32); else __syncthreads();
     const double t = tau[j];
-    if (t != 0.0) grp_update_cols<G>(m, j, x, t, A, lda, j + 1, K, wbeg * 32, nw * 32);
+    if (t != 0.0)  // ~8 rows per lane (measured best for the step-synchronous QR)
+      HMX_G_DISPATCH(m, (grp_update_cols<GG>(m, j, x, t, A, lda, j + 1, K, wbeg * 32, nw * 32)));
     if (bar) named_bar(bar, nw * 32); else __syncthreads();
   }
 }
 
 
-// G (lanes per column) from the row count: ~8 rows per lane.
-#define HMX_G_DISPATCH(m, CALL)            \
-  do {                                     \
-    if ((m) <= 64) { constexpr int GG = 8; CALL; }        \
-    else if ((m) <= 128) { constexpr int GG = 16; CALL; } \
-    else { constexpr int GG = 32; CALL; }                 \
-  } while (0)
-
 __device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau, double* red) {
-  HMX_G_DISPATCH(m, (qr_steps<GG>(m, K, A, lda, tau, 0, HMX_WARPS, 0)));
+  qr_steps(m, K, A, lda, tau, 0, HMX_WARPS, 0);
 }
 
 
@@ -347,7 +377,7 @@ __device__ void cta_householder_qr(int m, int K, double* A, int lda, double* tau
 // truncation) run concurrently in one CTA.
 __device__ void group_householder_qr(int m, int K, double* A, int lda, double* tau, int wbeg,
                                      int nw, int bar_id) {
-  HMX_G_DISPATCH(m, (qr_steps<GG>(m, K, A, lda, tau, wbeg, nw, bar_id)));
+  qr_steps(m, K, A, lda, tau, wbeg, nw, bar_id);
 }
 
 // X (m x r) := Q X where Q = H_0 H_1 ... H_{p-1} from cta_householder_qr.
@@ -370,7 +400,7 @@ __device__ void apply_q_cols(int m, int p, const double* A, int lda, const doubl
 
 __device__ void cta_apply_q(int m, int p, const double* A, int lda, const double* tau, int r,
                             double* X, int ldx) {
-  if (r > 0) HMX_G_DISPATCH(m, (apply_q_cols<GG>(m, p, A, lda, tau, r, X, ldx)));
+  if (r > 0) HMX_G_SWITCH(pick_g(m, r, HMX_THREADS), (apply_q_cols<GG>(m, p, A, lda, tau, r, X, ldx)));
   __syncthreads();
 }
 

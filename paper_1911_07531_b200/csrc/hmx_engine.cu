@@ -222,14 +222,15 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
                                const double* V, int ldv, const double* tau_v, double* Uo, int lduo,
                                double* Vo, int ldvo, double* colbuf) {
   const int grp = threadIdx.x / G, gl = threadIdx.x % G, ngrp = HMX_THREADS / G;
-  double* y = colbuf + (int64_t)grp * max(m, n);
+  double* ybuf = colbuf ? colbuf + (int64_t)grp * max(m, n) : nullptr;
   // U jobs and V jobs are issued in separate passes so that the reflector
   // loops of one pass have uniform trip counts across a warp
   for (int b = 0; b < r; b += ngrp) {
     const int c = b + grp;
     const bool act = c < r;
     double* yo = Uo + (int64_t)min(c, r - 1) * lduo;
-    if (act) for (int i = gl; i < m; i += G) y[i] = yo[i];
+    double* y = ybuf ? ybuf : yo;
+    if (act && ybuf) for (int i = gl; i < m; i += G) y[i] = yo[i];
     for (int j = kg - 1; j >= 0; --j) {
       const double t = tau_g[j];
       if (t != 0.0) grp_apply_reflector<G>(p, j, Gq + (int64_t)j * ldgq, t, y, gl, act);
@@ -238,18 +239,19 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
       const double t = tau_u[j];
       if (t != 0.0) grp_apply_reflector<G>(m, j, U + (int64_t)j * ldu, t, y, gl, act);
     }
-    if (act) for (int i = gl; i < m; i += G) yo[i] = y[i];
+    if (act && ybuf) for (int i = gl; i < m; i += G) yo[i] = y[i];
   }
   for (int b = 0; b < r; b += ngrp) {
     const int c = b + grp;
     const bool act = c < r;
     double* yo = Vo + (int64_t)min(c, r - 1) * ldvo;
-    if (act) for (int i = gl; i < n; i += G) y[i] = yo[i];
+    double* y = ybuf ? ybuf : yo;
+    if (act && ybuf) for (int i = gl; i < n; i += G) y[i] = yo[i];
     for (int j = q - 1; j >= 0; --j) {
       const double t = tau_v[j];
       if (t != 0.0) grp_apply_reflector<G>(n, j, V + (int64_t)j * ldv, t, y, gl, act);
     }
-    if (act) for (int i = gl; i < n; i += G) yo[i] = y[i];
+    if (act && ybuf) for (int i = gl; i < n; i += G) yo[i] = y[i];
   }
 }
 
@@ -293,8 +295,10 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   // stage U, V (and G) in shared memory when they fit
   const int64_t need = (int64_t)(m + n) * K + 2 * K + (int64_t)p * q;
   const int Lmn = max(m, n);
-  const int colneed = (Lmn <= 64 ? 32 : (Lmn <= 128 ? 16 : 8)) * Lmn;  // recomposition buffers
-  const bool stage = need + colneed <= kSmemWork;
+  const int gre = pick_g(Lmn, min(min(m, n), K), HMX_THREADS);  // recomposition groups (r <= K)
+  const int colneed = (HMX_THREADS / gre) * Lmn;
+  const bool stage = need <= kSmemWork;
+  const bool colsm = stage && need + colneed <= kSmemWork;  // column buffers fit too
   double* G;
   double* smw;
   int smcap;
@@ -354,8 +358,8 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     // fused recomposition: U columns get Q_G then Q_u, V columns Q_v; one
     // lane group per column job, no block barriers between reflectors
     // column buffers after G (X/J are dead by now): colneed doubles
-    double* colbuf = Gq + (int64_t)p * q;
-    HMX_G_DISPATCH(max(m, n), (recompose_jobs<GG>(r, p, q, m, n, kg, Gq, ldgq, tau_g, U, ldu_q, tau_u,
+    double* colbuf = colsm ? Gq + (int64_t)p * q : nullptr;
+    HMX_G_SWITCH(gre, (recompose_jobs<GG>(r, p, q, m, n, kg, Gq, ldgq, tau_g, U, ldu_q, tau_u,
                                                    V, ldv_q, tau_v, Uo, lduo, Vo, ldvo, colbuf)));
     __syncthreads();
   } else {
