@@ -26,13 +26,13 @@ _PLANS = {}
 
 
 def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0,
-             split_min=engine.DEFAULT_SPLIT_MIN):
+             split_min=engine.DEFAULT_SPLIT_MIN, nrep=1):
     """Cached execution plan (planning and upload happen once per tree)."""
-    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min)
+    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep)
     p = _PLANS.get(key)
     if p is None or p.table is not table:
         p = engine.ExecPlan(table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify,
-                            max_ctas=max_ctas, split_min=split_min)
+                            max_ctas=max_ctas, split_min=split_min, nrep=nrep)
         _PLANS[key] = p
     return p
 
@@ -63,6 +63,21 @@ def run_hlu(A, L, U, policy, mode, exec_mode=engine.EXEC_PERSISTENT, dag_mode=No
         if M.store.layout.rank_cap != rc:
             raise ValueError("L/U storage rank_cap differs from A's")
     plan = get_plan(t, mode, policy, rc, dag_mode, sparsify, split_min=split_min)
+    plan.run(A.store, L.store, U.store, exec_mode, stream)
+    c = plan.counters(stream)
+    counters.add(c["truncations"], c["updates"])
+    return plan
+
+
+def hlu_batch(A, L, U, policy: TruncationPolicy, mode="std", exec_mode=engine.EXEC_PERSISTENT,
+              stream=None, split_min=engine.DEFAULT_SPLIT_MIN):
+    """Factor every member of an HBatch (hmatrix.HBatch) in one launch;
+    mode "std" (arith.hlu semantics) or "accu" (accumulator.hlu_accu)."""
+    for M in (L, U):
+        if M.nrep != A.nrep or M.table is not A.table:
+            raise ValueError("batches differ in size or structure")
+    rc = A.store.layout.rank_cap
+    plan = get_plan(A.table, mode, policy, rc, split_min=split_min, nrep=A.nrep)
     plan.run(A.store, L.store, U.store, exec_mode, stream)
     c = plan.counters(stream)
     counters.add(c["truncations"], c["updates"])

@@ -55,6 +55,10 @@ class HStore:
     def clone(self):
         return HStore(self.layout, self.values.clone(), self.ranks.clone())
 
+    @property
+    def nrep(self):
+        return self.values.numel() // max(self.layout.size, 1)
+
     @classmethod
     def batch(cls, layout: Layout, nrep: int):
         """nrep same-layout matrices in one contiguous pool (batched plans)."""

@@ -303,3 +303,39 @@ def truncate(U, V, policy):
 __all__ = ["TruncationPolicy", "EXACT", "HMatrix", "assemble", "zeros", "from_leaves",
            "rel_error", "frobenius", "truncate", "dense_to_lowrank", "counters", "DENSE",
            "LOWRANK", "BLOCKED", "_lib"]
+
+
+class HBatch:
+    """R same-structure H-matrices in one contiguous device pool.
+
+    Factorizations of a batch run as ONE device launch over the disjoint
+    union of R copies of the lowered program (planner.replicate): the
+    single-matrix critical path leaves most SMs idle, a batch fills them.
+    """
+
+    def __init__(self, block: Block, policy=EXACT, nrep=1, rank_cap=DEFAULT_RANK_CAP, store=None):
+        from .engine import HStore
+
+        self.block = block
+        self.policy = policy
+        self.nrep = int(nrep)
+        t = table_of(block)
+        self.store = store if store is not None else HStore.batch(_layout(t, rank_cap), self.nrep)
+
+    @property
+    def table(self):
+        return self.store.table
+
+    def member(self, b: int) -> HMatrix:
+        return HMatrix(self.store.instance(b), self.block.uid, self.policy)
+
+    @classmethod
+    def replicate(cls, A: HMatrix, nrep: int) -> "HBatch":
+        """nrep copies of A (e.g. independent factorizations of one matrix)."""
+        out = cls(A.block, A.policy, nrep, A.store.layout.rank_cap)
+        for b in range(nrep):
+            out.store.instance(b).copy_from(A.store)
+        return out
+
+    def copy(self) -> "HBatch":
+        return HBatch(self.block, self.policy, self.nrep, store=self.store.clone())

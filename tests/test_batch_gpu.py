@@ -30,3 +30,26 @@ def test_c4_batch_ranks_match_reference():
         assert np.array_equal(ru[i][sel], arr["std_U_rank"][sel])
         tr += meta["std_truncations"]
     assert c["truncations"] == tr
+
+
+@pytest.mark.parametrize("mode", ["accu", "std"])
+def test_hbatch_replicas_equal_single(mode):
+    """A batch of R identical matrices factored in one launch gives, for
+    every member, the bits of the single factorization."""
+    from paper_1911_07531_b200 import configs, hmatrix as H
+    from paper_1911_07531_b200.arith import hlu_batch, run_hlu
+
+    cfg = configs.config("s2")
+    geom, root, perm, broot = configs.structure(cfg)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    A1 = A.copy()
+    L1, U1 = H.zeros(broot, pol, 64), H.zeros(broot, pol, 64)
+    run_hlu(A1, L1, U1, pol, mode)
+    R = 3
+    AB = H.HBatch.replicate(A, R)
+    LB, UB = H.HBatch(broot, pol, R, 64), H.HBatch(broot, pol, R, 64)
+    hlu_batch(AB, LB, UB, pol, mode)
+    for b in range(R):
+        assert np.array_equal(LB.member(b).store.values.cpu().numpy(), L1.store.values.cpu().numpy())
+        assert np.array_equal(UB.member(b).store.ranks.cpu().numpy(), U1.store.ranks.cpu().numpy())
