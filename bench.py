@@ -312,6 +312,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--instances", type=int, default=256, help="config 4 batch size (total)")
+    ap.add_argument("--ctas-per-sm", type=int, default=0,
+                    help="executor variant for the batched run (0 = auto: 2 when replicas > 1)")
     ap.add_argument("--replicas", type=int, default=8,
                     help="independent factorizations per GPU per step (throughput)")
     args = ap.parse_args()
@@ -396,7 +398,8 @@ def main():
     if R > 1:
         del A1, L1, U1
         t0 = time.time()
-        planR = get_plan(A0.table, cfg.mode, pol, args.rank_cap, nrep=R)
+        planR = get_plan(A0.table, cfg.mode, pol, args.rank_cap, nrep=R,
+                         ctas_per_sm=args.ctas_per_sm or None)
         setup["plan_batch_s"] = time.time() - t0
         AB0 = H.HBatch.replicate(A0, R)
         AB = H.HBatch(broot, pol, R, args.rank_cap)
@@ -486,7 +489,7 @@ def main():
         "config": {"workload": WORKLOADS.get(cfg.name, cfg.name), "n": int(cfg.n),
                    "mode": cfg.mode, "dag": plan1.dag_mode, "executor": args.exec,
                    "rank_cap": args.rank_cap,
-                   "replicas_per_gpu": R,
+                   "replicas_per_gpu": R, "ctas_per_sm": planT.ctas_per_sm,
                    "step": f"{R} independent factorizations of the config matrix per GPU "
                            "in one launch (replicated plan)",
                    "parallelism": f"replicas x{world}",

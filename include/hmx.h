@@ -130,7 +130,10 @@ typedef struct hmx_plan_desc {
   int32_t n_waves;
   int64_t scratch_doubles;    /* per-CTA scratch requirement                */
   int32_t scratch_ranks;      /* per-CTA rank-slot requirement              */
-  int32_t max_ctas;           /* 0 = 2 per SM                                */
+  int32_t max_ctas;           /* 0 = every SM x ctas_per_sm                  */
+  int32_t ctas_per_sm;        /* executor variant: 1 (160 KB shared memory,
+                                 255 registers; latency) or 2 (110 KB, 128
+                                 registers; batched throughput); 0 = 1     */
 } hmx_plan_desc;
 
 typedef struct hmx_plan* hmx_plan_t;

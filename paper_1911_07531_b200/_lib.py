@@ -58,6 +58,7 @@ class _PlanDesc(C.Structure):
         ("succ_ptr", C.c_void_p), ("succ_idx", C.c_void_p),
         ("wave_ptr", C.c_void_p), ("wave_tasks", C.c_void_p), ("n_waves", C.c_int32),
         ("scratch_doubles", C.c_int64), ("scratch_ranks", C.c_int32), ("max_ctas", C.c_int32),
+        ("ctas_per_sm", C.c_int32),
     ]
 
 
@@ -136,7 +137,7 @@ class Plan:
     """Owning handle of a device execution plan (hmx_plan_t)."""
 
     def __init__(self, ops, task_ops, succ_ptr, succ_idx, wave_ptr, wave_tasks,
-                 scratch_doubles, scratch_ranks, max_ctas=0):
+                 scratch_doubles, scratch_ranks, max_ctas=0, ctas_per_sm=1):
         L = lib()
         self._keep = [np.ascontiguousarray(ops, dtype=OP_DTYPE),
                       np.ascontiguousarray(task_ops, dtype=np.int64),
@@ -147,7 +148,7 @@ class Plan:
         o, to, sp, si, wp, wt = self._keep
         d = _PlanDesc(o.ctypes.data, len(o), to.ctypes.data, len(to) - 1, sp.ctypes.data,
                       si.ctypes.data, wp.ctypes.data, wt.ctypes.data, len(wp) - 1,
-                      int(scratch_doubles), int(scratch_ranks), int(max_ctas))
+                      int(scratch_doubles), int(scratch_ranks), int(max_ctas), int(ctas_per_sm))
         h = C.c_void_p()
         check(L.hmx_plan_create(C.byref(d), C.byref(h)), "plan_create")
         self.h = h
@@ -182,7 +183,9 @@ class Plan:
         check(lib().hmx_plan_trace(self.h, 1, out.ctypes.data_as(C.c_void_p)), "plan_trace")
         t = out[:3 * self.n_tasks].reshape(-1, 3)
         self.op_profile = out[3 * self.n_tasks:3 * self.n_tasks + 32].reshape(16, 2).astype(np.int64)
-        self.op_times = out[3 * self.n_tasks + 32:].astype(np.int64)
+        w = out[3 * self.n_tasks + 32:]
+        self.op_times = (w & np.uint64((1 << 40) - 1)).astype(np.int64)
+        self.op_inner = (w >> np.uint64(40)).astype(np.int64)  # resolved K of GEMM/TRUNC
         return t[:, 0].astype(np.int64), t[:, 1].astype(np.int64), (t[:, 2] & 0xffffffff).astype(np.int64)
 
     def close(self):

@@ -26,13 +26,15 @@ _PLANS = {}
 
 
 def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0,
-             split_min=engine.DEFAULT_SPLIT_MIN, nrep=1):
+             split_min=engine.DEFAULT_SPLIT_MIN, nrep=1, ctas_per_sm=None):
     """Cached execution plan (planning and upload happen once per tree)."""
-    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep)
+    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep,
+           ctas_per_sm)
     p = _PLANS.get(key)
     if p is None or p.table is not table:
         p = engine.ExecPlan(table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify,
-                            max_ctas=max_ctas, split_min=split_min, nrep=nrep)
+                            max_ctas=max_ctas, split_min=split_min, nrep=nrep,
+                            ctas_per_sm=ctas_per_sm)
         _PLANS[key] = p
     return p
 
@@ -70,14 +72,18 @@ def run_hlu(A, L, U, policy, mode, exec_mode=engine.EXEC_PERSISTENT, dag_mode=No
 
 
 def hlu_batch(A, L, U, policy: TruncationPolicy, mode="std", exec_mode=engine.EXEC_PERSISTENT,
-              stream=None, split_min=engine.DEFAULT_SPLIT_MIN):
+              stream=None, split_min=engine.DEFAULT_SPLIT_MIN, ctas_per_sm=None):
     """Factor every member of an HBatch (hmatrix.HBatch) in one launch;
-    mode "std" (arith.hlu semantics) or "accu" (accumulator.hlu_accu)."""
+    mode "std" (arith.hlu semantics) or "accu" (accumulator.hlu_accu).
+    ctas_per_sm selects the executor variant (default: 2 for R > 1, see
+    engine.ExecPlan); with 1 every member reproduces the bits of a single
+    arith.hlu / hlu_accu run."""
     for M in (L, U):
         if M.nrep != A.nrep or M.table is not A.table:
             raise ValueError("batches differ in size or structure")
     rc = A.store.layout.rank_cap
-    plan = get_plan(A.table, mode, policy, rc, split_min=split_min, nrep=A.nrep)
+    plan = get_plan(A.table, mode, policy, rc, split_min=split_min, nrep=A.nrep,
+                    ctas_per_sm=ctas_per_sm)
     plan.run(A.store, L.store, U.store, exec_mode, stream)
     c = plan.counters(stream)
     counters.add(c["truncations"], c["updates"])

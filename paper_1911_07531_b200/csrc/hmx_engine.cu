@@ -47,10 +47,15 @@ enum OpCode : int32_t {
 enum : int32_t { F_TA = 1, F_TB = 2, F_ACC = 4 };
 
 constexpr int kScratchBase = 15;
-constexpr int kSmemDoubles = 20480;  // 160 KB dynamic shared memory (leaves ~68 KB of L1), 1 CTA per SM
-constexpr int kSmemWork = kSmemDoubles - 32;
+// Two residency variants of every executor kernel (a plan picks one):
+// 1 CTA per SM: 160 KB dynamic shared memory (leaves ~68 KB of L1) and up
+// to 255 registers -- lowest latency per op (single factorizations);
+// 2 CTAs per SM: 110 KB each, registers capped at 128 -- one CTA's
+// barrier/shuffle latency hides behind the other's (batched throughput).
+__host__ __device__ constexpr int smem_doubles(int occ) { return occ == 1 ? 20480 : 14080; }
 
 struct DevPlan {
+  int smem_work;  // usable dynamic shared memory (doubles) of the launched variant
   const hmx_op* ops;
   const int64_t* task_ops;
   double* bases[16];
@@ -297,8 +302,8 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   const int Lmn = max(m, n);
   const int gre = pick_g(Lmn, min(min(m, n), K), HMX_THREADS);  // recomposition groups (r <= K)
   const int colneed = (HMX_THREADS / gre) * Lmn;
-  const bool stage = need <= kSmemWork;
-  const bool colsm = stage && need + colneed <= kSmemWork;  // column buffers fit too
+  const bool stage = need <= P.smem_work;
+  const bool colsm = stage && need + colneed <= P.smem_work;  // column buffers fit too
   double* G;
   double* smw;
   int smcap;
@@ -326,21 +331,21 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     }
     __syncthreads();
     smw = G + p * q;
-    smcap = (int)(kSmemWork - need);
+    smcap = (int)(P.smem_work - need);
   } else {
-    cta_qr_blocked(m, K, U, ldu, tau_u, Vxu, m, Tu, Wq, work, kSmemWork, red);
-    cta_qr_blocked(n, K, V, ldv, tau_v, Vxv, n, Tv, Wq, work, kSmemWork, red);
+    cta_qr_blocked(m, K, U, ldu, tau_u, Vxu, m, Tu, Wq, work, P.smem_work, red);
+    cta_qr_blocked(n, K, V, ldv, tau_v, Vxv, n, Tv, Wq, work, P.smem_work, red);
     FOR_MN(i, l, p, K) Ruz[i + l * p] = (l >= i) ? U[i + (int64_t)l * ldu] : 0.0;
     FOR_MN(i, l, q, K) Rvz[i + l * q] = (l >= i) ? V[i + (int64_t)l * ldv] : 0.0;
     // shared memory goes to the Jacobi factors first (X q x k, J k x k);
     // the core G lives there too only when all three fit
     const int s_ = min(p, q);
-    const bool gsm = p * q + q * s_ + s_ * s_ + GEMM_SMEM_DOUBLES <= kSmemWork;
+    const bool gsm = p * q + q * s_ + s_ * s_ + GEMM_SMEM_DOUBLES <= P.smem_work;
     G = gsm ? work : Gg;
     __syncthreads();
     cta_gemm(p, q, K, 1.0, Ruz, p, false, Rvz, q, true, false, G, p, gsm ? work + p * q : work);
     smw = gsm ? work + p * q : work;
-    smcap = gsm ? kSmemWork - p * q : kSmemWork;
+    smcap = gsm ? P.smem_work - p * q : P.smem_work;
   }
   const int ldu_q = stage ? m : ldu, ldv_q = stage ? n : ldv;
   phase(P, 12, tq);
@@ -348,7 +353,7 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* tau_g = nullptr;
   int ldgq = 0, kg = 0;
   const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm, nullptr,
-                            (!stage && G != Gg) ? Gg : nullptr, p, work, kSmemWork,
+                            (!stage && G != Gg) ? Gg : nullptr, p, work, P.smem_work,
                             stage ? &Gq : nullptr, &ldgq, &tau_g, &kg);
   if (P.trace && threadIdx.x == 0) tq = gtimer2();
   FOR_MN(i, t, m - p, r) Uo[p + i + (int64_t)t * lduo] = 0.0;
@@ -363,8 +368,8 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
                                                    V, ldv_q, tau_v, Uo, lduo, Vo, ldvo, colbuf)));
     __syncthreads();
   } else {
-    cta_apply_q_blocked(m, p, Vxu, m, Tu, r, Uo, lduo, Wq, work, kSmemWork);
-    cta_apply_q_blocked(n, q, Vxv, n, Tv, r, Vo, ldvo, Wq, work, kSmemWork);
+    cta_apply_q_blocked(m, p, Vxu, m, Tu, r, Uo, lduo, Wq, work, P.smem_work);
+    cta_apply_q_blocked(n, q, Vxv, n, Tv, r, Vo, ldvo, Wq, work, P.smem_work);
   }
   phase(P, 15, tq);
   if (threadIdx.x == 0) *rslot = r;
@@ -389,7 +394,7 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* work = sm + 32;
   double* G = M;
   int ldg = ldm;
-  const bool gsm = m * n + 64 <= kSmemWork;
+  const bool gsm = m * n + 64 <= P.smem_work;
   if (gsm) {
     G = work;
     ldg = m;
@@ -397,9 +402,9 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
     __syncthreads();
   }
   double* smw = gsm ? work + m * n : work;
-  const int smcap = gsm ? kSmemWork - m * n : kSmemWork;
+  const int smcap = gsm ? P.smem_work - m * n : P.smem_work;
   const int r = svd_lowrank(P, o, m, n, G, ldg, ws, smw, smcap, Uo, o.ld[2], Vo, o.ld[3], sm,
-                            nullptr, gsm ? M : nullptr, ldm, work, kSmemWork);
+                            nullptr, gsm ? M : nullptr, ldm, work, P.smem_work);
   if (threadIdx.x == 0) *rslot = r;
   const int s = min(m, n);
   count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s + (double)s * n));
@@ -415,7 +420,7 @@ __device__ void op_svals(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   for (int e = threadIdx.x; e < p * q; e += HMX_THREADS)
     W[e] = G[(e % p) + (int64_t)(e / p) * o.ld[0]];
   __syncthreads();
-  svd_lowrank(P, o, p, q, W, p, ws, sm + 32, kSmemWork, nullptr, 0, nullptr, 0, sm, out);
+  svd_lowrank(P, o, p, q, W, p, ws, sm + 32, P.smem_work, nullptr, 0, nullptr, 0, sm, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -461,7 +466,7 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
     case OP_LU: {
       const int n = o.dim[0];
       double* U = mref(P, c, o.ref[2]);
-      double* W = (n * n + n <= kSmemWork) ? work + n : U;
+      double* W = (n * n + n <= P.smem_work) ? work + n : U;
       const bool ok = cta_lu(n, mref(P, c, o.ref[0]), o.ld[0], mref(P, c, o.ref[1]), o.ld[1], U,
                              o.ld[2], W, work, red);
       if (!ok && threadIdx.x == 0) set_status(P, HMX_ERR_PIVOT);
@@ -477,14 +482,14 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       double* B = mref(P, c, o.ref[2]);
       int ldb = o.ld[2];
       double* Ts = work;
-      const bool stageT = n * n <= kSmemWork;
+      const bool stageT = n * n <= P.smem_work;
       if (stageT) {
         FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];
         T = Ts;
         ldt = n;
       }
       double* Bs = work + (stageT ? n * n : 0);
-      const bool stageB = stageT && (n * n + n * cc <= kSmemWork);
+      const bool stageB = stageT && (n * n + n * cc <= P.smem_work);
       if (stageB) FOR_MN(i, j, n, cc) Bs[i + j * n] = B[i + (int64_t)j * ldb];
       __syncthreads();
       double* Bw = stageB ? Bs : B;
@@ -561,8 +566,12 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
   const int64_t b = P.task_ops[t], e = P.task_ops[t + 1];
   for (int64_t i = b; i < e; ++i) {
     const hmx_op o = P.ops[i];
-    unsigned long long q0 = 0;
-    if (P.trace && threadIdx.x == 0) q0 = gtimer();
+    unsigned long long q0 = 0, kin = 0;
+    if (P.trace && threadIdx.x == 0) {
+      q0 = gtimer();
+      // resolved inner dimension (K of GEMM / TRUNC) for shape histograms
+      if (o.code == OP_TRUNC || o.code == OP_GEMM) kin = (unsigned long long)min(dimv(P, c, o.dim[2]), 4095);
+    }
     run_op(P, c, o, sm);
     if (P.trace && threadIdx.x == 0) {
       // per-opcode busy time and count, after the task records (3*n_tasks
@@ -571,7 +580,7 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
       const unsigned long long dt = gtimer() - q0;
       atomicAdd(&prof[2 * (o.code & 15)], dt);
       atomicAdd(&prof[2 * (o.code & 15) + 1], 1ull);
-      prof[32 + i] = dt;
+      prof[32 + i] = (dt & ((1ull << 40) - 1)) | (kin << 40);
     }
   }
   if (threadIdx.x == 0) {
@@ -584,7 +593,8 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
   }
 }
 
-__global__ void __launch_bounds__(HMX_THREADS, 1) k_tasks(DevPlan P, const int* tasks, int ntasks) {
+template <int OCC>
+__global__ void __launch_bounds__(HMX_THREADS, OCC) k_tasks(DevPlan P, const int* tasks, int ntasks) {
   extern __shared__ double sm[];
   for (int i = blockIdx.x; i < ntasks; i += gridDim.x) {
     run_task(P, tasks ? tasks[i] : i, sm);
@@ -594,7 +604,8 @@ __global__ void __launch_bounds__(HMX_THREADS, 1) k_tasks(DevPlan P, const int* 
 
 __device__ __forceinline__ int ld_relaxed(int* p) { return atomicAdd(p, 0); }
 
-__global__ void __launch_bounds__(HMX_THREADS, 1) k_persistent(DevPlan P) {
+template <int OCC>
+__global__ void __launch_bounds__(HMX_THREADS, OCC) k_persistent(DevPlan P) {
   extern __shared__ double sm[];
   __shared__ int s_task;
   for (;;) {
@@ -688,11 +699,11 @@ int num_sms() {
 bool g_attr_set = false;
 cudaError_t set_attrs() {
   if (g_attr_set) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmemDoubles * (int)sizeof(double));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSmemDoubles * (int)sizeof(double));
+  const int b1 = smem_doubles(1) * (int)sizeof(double), b2 = smem_doubles(2) * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_tasks<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b1);
+  if (!e) e = cudaFuncSetAttribute(k_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b1);
+  if (!e) e = cudaFuncSetAttribute(k_tasks<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+  if (!e) e = cudaFuncSetAttribute(k_persistent<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
   if (e != cudaSuccess) return e;
   g_attr_set = true;
   return cudaSuccess;
@@ -725,6 +736,7 @@ struct hmx_plan {
   int64_t scratch_stride = 0;
   int rscratch_stride = 0;
   int n_ctas = 0;
+  int occ = 1;  // CTAs per SM of the executor variant (1 or 2)
   unsigned long long* d_counters = nullptr;
   int* d_status = nullptr;
   double* bases[16] = {};
@@ -762,6 +774,7 @@ DevPlan make_dev(hmx_plan* p) {
   P.qctl = p->d_qctl;
   P.n_tasks = p->n_tasks;
   P.trace = p->d_trace;
+  P.smem_work = smem_doubles(p->occ) - 32;
   return P;
 }
 
@@ -775,12 +788,13 @@ hmx_status cuda_status(cudaError_t e) {
 
 cudaError_t launch_waves(hmx_plan* p, cudaStream_t s) {
   DevPlan P = make_dev(p);
-  const size_t smem = kSmemDoubles * sizeof(double);
+  const size_t smem = smem_doubles(p->occ) * sizeof(double);
   for (int w = 0; w < p->n_waves; ++w) {
     const int b = p->wave_ptr[w], n = p->wave_ptr[w + 1] - b;
     if (!n) continue;
     const int grid = std::min(n, p->n_ctas);
-    k_tasks<<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
+    if (p->occ == 2) k_tasks<2><<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
+    else k_tasks<1><<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
   }
   return cudaGetLastError();
 }
@@ -829,7 +843,16 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   std::vector<int> seq(nt);
   for (int i = 0; i < nt; ++i) seq[i] = i;
   if (!e) e = upload(&p->d_seq_tasks, seq.data(), (size_t)nt);
-  p->n_ctas = d->max_ctas > 0 ? d->max_ctas : num_sms();
+  p->occ = d->ctas_per_sm == 2 ? 2 : 1;
+  p->n_ctas = d->max_ctas > 0 ? d->max_ctas : num_sms() * p->occ;
+  {  // the persistent scheduler spins: every CTA of its grid must be resident
+    int occ = 0;
+    const size_t bytes = smem_doubles(p->occ) * sizeof(double);
+    const cudaError_t eo =
+        p->occ == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent<2>, HMX_THREADS, bytes)
+                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent<1>, HMX_THREADS, bytes);
+    if (eo == cudaSuccess && occ > 0) p->n_ctas = std::min(p->n_ctas, occ * num_sms());
+  }
   p->scratch_stride = std::max<int64_t>(d->scratch_doubles, 1);
   p->scratch_stride = (p->scratch_stride + 31) & ~int64_t(31);
   p->rscratch_stride = std::max(d->scratch_ranks, 1);
@@ -859,7 +882,7 @@ hmx_status hmx_plan_execute(hmx_plan_t p, int32_t mode, void* stream) {
   if (!p) return HMX_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   if (p->n_tasks == 0) return HMX_OK;
-  const size_t smem = kSmemDoubles * sizeof(double);
+  const size_t smem = smem_doubles(p->occ) * sizeof(double);
   cudaError_t e = cudaSuccess;
   if (mode == 0) {
     e = launch_waves(p, s);
@@ -890,13 +913,15 @@ hmx_status hmx_plan_execute(hmx_plan_t p, int32_t mode, void* stream) {
     if (!e) e = cudaMemcpyAsync(p->d_qctl, p->qctl_init, 2 * sizeof(int), cudaMemcpyHostToDevice, s);
     if (!e) {
       DevPlan P = make_dev(p);
-      k_persistent<<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
+      if (p->occ == 2) k_persistent<2><<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
+      else k_persistent<1><<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
       e = cudaGetLastError();
     }
   } else if (mode == 3) {
     DevPlan P = make_dev(p);
     for (int t = 0; t < p->n_tasks && !e; ++t) {
-      k_tasks<<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
+      if (p->occ == 2) k_tasks<2><<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
+      else k_tasks<1><<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
       e = cudaGetLastError();
     }
   } else {

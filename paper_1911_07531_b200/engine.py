@@ -152,7 +152,8 @@ class ExecPlan:
     """Lowered H-LU plan + its device execution graph."""
 
     def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
-                 sparsify=False, max_ctas=0, nrep=1, split_min=DEFAULT_SPLIT_MIN):
+                 sparsify=False, max_ctas=0, nrep=1, split_min=DEFAULT_SPLIT_MIN,
+                 ctas_per_sm=None):
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
         self.table = table
@@ -198,8 +199,11 @@ class ExecPlan:
         counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
         self.wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.wave_tasks = order
+        # executor variant: one CTA per SM (latency) for a single matrix, two
+        # per SM (throughput) for a batch of independent instances
+        self.ctas_per_sm = int(ctas_per_sm or (2 if self.nrep > 1 else 1))
         self.plan = _lib.Plan(ops, task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
-                              prog.scratch_doubles, prog.scratch_ranks, max_ctas)
+                              prog.scratch_doubles, prog.scratch_ranks, max_ctas, self.ctas_per_sm)
         torch = _torch()
         self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")

@@ -49,7 +49,18 @@ def test_hbatch_replicas_equal_single(mode):
     R = 3
     AB = H.HBatch.replicate(A, R)
     LB, UB = H.HBatch(broot, pol, R, 64), H.HBatch(broot, pol, R, 64)
-    hlu_batch(AB, LB, UB, pol, mode)
+    hlu_batch(AB, LB, UB, pol, mode, ctas_per_sm=1)
     for b in range(R):
         assert np.array_equal(LB.member(b).store.values.cpu().numpy(), L1.store.values.cpu().numpy())
         assert np.array_equal(UB.member(b).store.ranks.cpu().numpy(), U1.store.ranks.cpu().numpy())
+    # the two-CTAs-per-SM variant (110 KB shared memory: other staging
+    # decisions, other rounding) keeps every rank and the factors to 1e-9
+    AB = H.HBatch.replicate(A, R)
+    LB, UB = H.HBatch(broot, pol, R, 64), H.HBatch(broot, pol, R, 64)
+    hlu_batch(AB, LB, UB, pol, mode, ctas_per_sm=2)
+    for b in range(R):
+        for X, X1 in ((LB, L1), (UB, U1)):
+            assert np.array_equal(X.member(b).store.ranks.cpu().numpy(), X1.store.ranks.cpu().numpy())
+            d1 = X1.to_dense()
+            d = X.member(b).to_dense()
+            assert np.linalg.norm(d - d1) <= 1e-9 * np.linalg.norm(d1)
