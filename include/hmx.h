@@ -142,8 +142,10 @@ hmx_status hmx_plan_create(const hmx_plan_desc* desc, hmx_plan_t* out);
 /* Bind device storage for base id 0..14 (matrix pools) and rank arrays. */
 hmx_status hmx_plan_bind(hmx_plan_t plan, int32_t base_id, double* values, int32_t* ranks);
 /* Execute: mode 0 = wavefront launches, 1 = wavefronts captured in a CUDA
- * graph, 2 = persistent kernel with device dependency counters,
- * 3 = sequential (one task per launch, debugging). */
+ * graph, 2 = persistent kernel with device dependency counters (cooperative
+ * launch: every CTA resident), 3 = sequential (one task per launch,
+ * debugging), 4 = persistent kernel without resetting the scheduler state
+ * (partitioned runs, after hmx_plan_reset on every rank). */
 hmx_status hmx_plan_execute(hmx_plan_t plan, int32_t mode, void* stream);
 /* Synchronise `stream` and fetch the device status word (HMX_ERR_* bits). */
 hmx_status hmx_plan_status(hmx_plan_t plan, void* stream, int32_t* status_bits);
@@ -158,6 +160,54 @@ hmx_status hmx_plan_reset_counters(hmx_plan_t plan, void* stream);
  * (3*n_tasks + 32 + n_ops words). */
 hmx_status hmx_plan_trace(hmx_plan_t plan, int32_t enable, uint64_t* out);
 hmx_status hmx_plan_destroy(hmx_plan_t plan);
+
+/* ------------------------------------------------------------------------
+ * Block-row partitioned execution over NVLink peer memory (SURVEY.md §8e:
+ * Owner(block) = owner of its row cluster; one exchange per cross-rank DAG
+ * edge).  The reference has no multi-node executor; its task DAG
+ * (taskgraph.py:636-665) is what gets partitioned.  A task's CTA, after the
+ * task, copies the objects a task of another rank reads next into that
+ * rank's storage (hmx_pub records), fences system-wide, then releases its
+ * successors in their owners' scheduler state (remote atomics).
+ * ---------------------------------------------------------------------- */
+typedef struct hmx_pub {
+  int32_t kind;      /* 0: len doubles; 1: low-rank leaf (m x rk and n x rk, rk from the rank word) */
+  int32_t dst;       /* destination rank                                       */
+  int32_t base;      /* matrix pool id (0..14)                                 */
+  int32_t rbase;     /* rank-array id of the object's rank word                */
+  int64_t src_off;   /* element offsets in the source / destination pools      */
+  int64_t dst_off;
+  int64_t src_off2;  /* kind 1: V factor offsets                               */
+  int64_t dst_off2;
+  int64_t len;       /* kind 0: doubles                                        */
+  int32_t m, n;      /* kind 1: rows of U and V                                */
+  int32_t src_ridx;  /* rank word index (-1: none)                             */
+  int32_t dst_ridx;
+} hmx_pub; /* 72 bytes */
+
+/* Attach a partition to a plan.  rank = -1: every rank is emulated by this
+ * one launch (CTA c serves rank c % nranks; the ranks' storage replicas
+ * live in the bound pools at the offsets the ops and records carry).
+ * rank >= 0: this process is that rank; the other ranks' storage and
+ * scheduler state are attached with hmx_plan_peer.  owner[n_tasks];
+ * pub_ptr[n_tasks + 1] prefix offsets into pub[n_pub]. */
+hmx_status hmx_plan_partition(hmx_plan_t plan, int32_t nranks, int32_t rank, const int32_t* owner,
+                              const int64_t* pub_ptr, const hmx_pub* pub, int64_t n_pub);
+/* Device addresses of this plan's scheduler state (in-degrees [n_tasks],
+ * ready queue [n_tasks], queue control [2]) for export to peers. */
+hmx_status hmx_plan_sched_state(hmx_plan_t plan, void** indeg, void** queue, void** qctl);
+/* Storage (16 pools + 16 rank arrays) and scheduler state of rank r, as
+ * mapped into this process (hmx_ipc_open). */
+hmx_status hmx_plan_peer(hmx_plan_t plan, int32_t r, double* const* bases, int32_t* const* rbases,
+                         int32_t* indeg, int32_t* queue, int32_t* qctl);
+/* Reset the scheduler state to its initial values (every rank resets and
+ * synchronises before any rank launches with execute mode 4). */
+hmx_status hmx_plan_reset(hmx_plan_t plan, void* stream);
+/* CUDA IPC of device allocations: handle (64 bytes) of the allocation that
+ * contains dptr and dptr's offset in it; open maps a peer's allocation. */
+hmx_status hmx_ipc_handle(const void* dptr, void* handle, int64_t* offset);
+hmx_status hmx_ipc_open(const void* handle, void** base);
+hmx_status hmx_ipc_close(void* base);
 
 /* Dense evaluation of the exponential point kernel used by the BASELINE
  * configs (problems.PointKernel problems.py:43-53 + permuted 78-81):

@@ -97,6 +97,13 @@ def lib():
         "hmx_plan_trace": ([vp, i32, vp], i32),
         "hmx_exp_kernel_blocks": ([i32, vp, vp, i32, vp, f64, f64, f64, vp, vp], i32),
         "hmx_fp64_fma_probe": ([i32, i32, vp, vp], i32),
+        "hmx_plan_partition": ([vp, i32, i32, vp, vp, vp, i64], i32),
+        "hmx_plan_sched_state": ([vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)], i32),
+        "hmx_plan_peer": ([vp, i32, vp, vp, vp, vp, vp], i32),
+        "hmx_plan_reset": ([vp, vp], i32),
+        "hmx_ipc_handle": ([vp, vp, C.POINTER(i64)], i32),
+        "hmx_ipc_open": ([vp, C.POINTER(vp)], i32),
+        "hmx_ipc_close": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -114,7 +121,30 @@ EXPORTED = (
     "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
     "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_plan_trace", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",
+    "hmx_plan_partition", "hmx_plan_sched_state", "hmx_plan_peer", "hmx_plan_reset",
+    "hmx_ipc_handle", "hmx_ipc_open", "hmx_ipc_close",
 )
+
+
+def ipc_handle(ptr):
+    """(64-byte CUDA IPC handle of the allocation holding device address
+    ptr, ptr's byte offset in it)."""
+    h = (C.c_uint8 * 64)()
+    off = C.c_int64()
+    check(lib().hmx_ipc_handle(C.c_void_p(int(ptr)), h, C.byref(off)), "ipc_handle")
+    return bytes(h), int(off.value)
+
+
+def ipc_open(handle: bytes):
+    """Map a peer allocation; returns its base address in this process."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    base = C.c_void_p()
+    check(lib().hmx_ipc_open(h, C.byref(base)), "ipc_open")
+    return int(base.value)
+
+
+def ipc_close(base):
+    check(lib().hmx_ipc_close(C.c_void_p(int(base))), "ipc_close")
 
 
 def check(status, what=""):
@@ -158,6 +188,29 @@ class Plan:
 
     def bind(self, base_id, values, ranks=None):
         check(lib().hmx_plan_bind(self.h, int(base_id), ptr(values), ptr(ranks)), "plan_bind")
+
+    def partition(self, nranks, rank, owner, pub_ptr, pub):
+        """Attach a block-row partition (hmx_plan_partition)."""
+        o = np.ascontiguousarray(owner, dtype=np.int32)
+        pp = np.ascontiguousarray(pub_ptr, dtype=np.int64)
+        pb = np.ascontiguousarray(pub)
+        check(lib().hmx_plan_partition(self.h, int(nranks), int(rank), o.ctypes.data, pp.ctypes.data,
+                                       pb.ctypes.data if len(pb) else None, len(pb)), "plan_partition")
+
+    def sched_state(self):
+        a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib().hmx_plan_sched_state(self.h, C.byref(a), C.byref(b), C.byref(c)), "sched_state")
+        return int(a.value or 0), int(b.value or 0), int(c.value or 0)
+
+    def peer(self, r, bases, rbases, indeg, queue, qctl):
+        """Storage (16 pool + 16 rank-array addresses) and scheduler state of rank r."""
+        bb = (C.c_void_p * 16)(*[int(x or 0) for x in bases])
+        rb = (C.c_void_p * 16)(*[int(x or 0) for x in rbases])
+        check(lib().hmx_plan_peer(self.h, int(r), bb, rb, C.c_void_p(int(indeg)), C.c_void_p(int(queue)),
+                                  C.c_void_p(int(qctl))), "plan_peer")
+
+    def reset(self, stream=None):
+        check(lib().hmx_plan_reset(self.h, stream_ptr(stream)), "plan_reset")
 
     def execute(self, mode=2, stream=None):
         check(lib().hmx_plan_execute(self.h, int(mode), stream_ptr(stream)), "plan_execute")

@@ -74,6 +74,18 @@ struct DevPlan {
   int* qctl;  // [0] head, [1] tail
   int n_tasks;
   unsigned long long* trace;  // optional: per task (start ns, end ns, smid)
+  // block-row partition over ranks (hmx_plan_partition); nranks == 1: off
+  int nranks;
+  int rank;                   // this process's rank, or -1: every rank emulated in one launch
+  const int* owner;           // [n_tasks] owning rank of each task
+  const int* n_local;         // [nranks] tasks owned by each rank
+  int* const* r_indeg;        // [nranks] scheduler state of every rank (peer pointers)
+  int* const* r_queue;
+  int* const* r_qctl;
+  double* const* r_bases;     // [nranks * 16] storage of every rank (peer pointers)
+  int* const* r_rbases;
+  const int64_t* pub_ptr;     // [n_tasks + 1] CSR of the copies a finished task publishes
+  const hmx_pub* pub;
 };
 
 struct Cx {
@@ -604,17 +616,48 @@ __global__ void __launch_bounds__(HMX_THREADS, OCC) k_tasks(DevPlan P, const int
 
 __device__ __forceinline__ int ld_relaxed(int* p) { return atomicAdd(p, 0); }
 
+// Copies task t's outputs into the storage of the ranks that read them next
+// (hmx_pub records, built by partition.py from the program's data-access
+// records), then makes them visible system-wide before successors are
+// released.  Peer storage is NVLink-mapped device memory of the other GPUs
+// (or, emulated, other replicas in this GPU's pools).
+__device__ void publish(const DevPlan& P, int my, int t) {
+  const int64_t b = P.pub_ptr[t], e = P.pub_ptr[t + 1];
+  if (b == e) return;
+  for (int64_t k = b; k < e; ++k) {
+    const hmx_pub r = P.pub[k];
+    const double* src = P.r_bases[my * 16 + r.base];
+    double* dst = P.r_bases[r.dst * 16 + r.base];
+    int64_t len = r.len, len2 = 0;
+    if (r.kind == 1) {  // low-rank leaf: only the live rank columns move
+      const int rk = P.r_rbases[my * 16 + r.rbase][r.src_ridx];
+      len = (int64_t)r.m * rk;
+      len2 = (int64_t)r.n * rk;
+    }
+    for (int64_t i = threadIdx.x; i < len; i += HMX_THREADS) dst[r.dst_off + i] = src[r.src_off + i];
+    for (int64_t i = threadIdx.x; i < len2; i += HMX_THREADS) dst[r.dst_off2 + i] = src[r.src_off2 + i];
+    if (r.src_ridx >= 0 && threadIdx.x == 0)
+      P.r_rbases[r.dst * 16 + r.rbase][r.dst_ridx] = P.r_rbases[my * 16 + r.rbase][r.src_ridx];
+  }
+  __threadfence_system();
+}
+
 template <int OCC>
 __global__ void __launch_bounds__(HMX_THREADS, OCC) k_persistent(DevPlan P) {
   extern __shared__ double sm[];
   __shared__ int s_task;
+  // partitioned: this CTA serves rank `my` (its own queue, tasks, storage)
+  const int my = P.nranks > 1 ? (P.rank >= 0 ? P.rank : (int)(blockIdx.x % P.nranks)) : 0;
+  int* const queue = P.nranks > 1 ? P.r_queue[my] : P.queue;
+  int* const qctl = P.nranks > 1 ? P.r_qctl[my] : P.qctl;
+  const int nloc = P.nranks > 1 ? P.n_local[my] : P.n_tasks;
   for (;;) {
     if (threadIdx.x == 0) {
-      const int slot = atomicAdd(&P.qctl[0], 1);
+      const int slot = atomicAdd(&qctl[0], 1);
       int t = -1;
-      if (slot < P.n_tasks) {
+      if (slot < nloc) {
         long long spins = 0;
-        while ((t = ld_relaxed(&P.queue[slot])) < 0) {
+        while ((t = ld_relaxed(&queue[slot])) < 0) {
           __nanosleep(128);
           if (++spins > (1ll << 27)) { atomicOr(P.status, HMX_ERR_TIMEOUT); t = -2; break; }
           if ((spins & 1023) == 0 && (ld_relaxed(P.status) & HMX_ERR_TIMEOUT)) { t = -2; break; }
@@ -629,7 +672,21 @@ __global__ void __launch_bounds__(HMX_THREADS, OCC) k_persistent(DevPlan P) {
     run_task(P, t, sm);
     __threadfence();  // release this task's outputs (every writer thread)
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (P.nranks > 1) {
+      publish(P, my, t);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int k = P.succ_ptr[t]; k < P.succ_ptr[t + 1]; ++k) {
+          const int s = P.succ_idx[k];
+          const int r = P.owner[s];
+          if (atomicSub(&P.r_indeg[r][s], 1) == 1) {
+            const int pos = atomicAdd(&P.r_qctl[r][1], 1);
+            atomicExch(&P.r_queue[r][pos], s);
+          }
+        }
+      }
+    } else if (threadIdx.x == 0) {
       __threadfence();
       for (int k = P.succ_ptr[t]; k < P.succ_ptr[t + 1]; ++k) {
         const int s = P.succ_idx[k];
@@ -743,6 +800,23 @@ struct hmx_plan {
   int* rbases[16] = {};
   cudaGraphExec_t gexec = nullptr;
   unsigned long long* d_trace = nullptr;
+  // host copies for partitioning
+  std::vector<int> indeg_h, wave_tasks_h;
+  // partition (hmx_plan_partition); nranks == 1: none
+  int nranks = 1, rank = 0;
+  int* d_owner = nullptr;
+  int* d_n_local = nullptr;
+  int64_t* d_pub_ptr = nullptr;
+  hmx_pub* d_pub = nullptr;
+  std::vector<int> qctl_init_v;                 // 2 per emulated rank (2 for a real rank)
+  std::vector<double*> h_r_bases;               // nranks * 16 (own entries refreshed at launch)
+  std::vector<int*> h_r_rbases;
+  std::vector<int*> h_r_indeg, h_r_queue, h_r_qctl;
+  double** d_r_bases = nullptr;
+  int** d_r_rbases = nullptr;
+  int** d_r_indeg = nullptr;
+  int** d_r_queue = nullptr;
+  int** d_r_qctl = nullptr;
 };
 
 namespace {
@@ -775,6 +849,19 @@ DevPlan make_dev(hmx_plan* p) {
   P.n_tasks = p->n_tasks;
   P.trace = p->d_trace;
   P.smem_work = smem_doubles(p->occ) - 32;
+  P.nranks = p->nranks;
+  P.rank = p->rank;
+  if (p->nranks > 1) {
+    P.owner = p->d_owner;
+    P.n_local = p->d_n_local;
+    P.r_indeg = p->d_r_indeg;
+    P.r_queue = p->d_r_queue;
+    P.r_qctl = p->d_r_qctl;
+    P.r_bases = p->d_r_bases;
+    P.r_rbases = p->d_r_rbases;
+    P.pub_ptr = p->d_pub_ptr;
+    P.pub = p->d_pub;
+  }
   return P;
 }
 
@@ -784,6 +871,39 @@ hmx_status cuda_status(cudaError_t e) {
     return HMX_ERR_CUDA;
   }
   return HMX_OK;
+}
+
+cudaError_t reset_sched(hmx_plan* p, cudaStream_t s) {
+  const size_t qn = (p->nranks > 1 && p->rank < 0) ? (size_t)p->nranks * p->n_tasks : (size_t)p->n_tasks;
+  cudaError_t e = cudaMemcpyAsync(p->d_indeg, p->d_indeg_init, p->n_tasks * sizeof(int),
+                                  cudaMemcpyDeviceToDevice, s);
+  if (!e) e = cudaMemcpyAsync(p->d_queue, p->d_queue_init, qn * sizeof(int), cudaMemcpyDeviceToDevice, s);
+  if (!e)
+    e = cudaMemcpyAsync(p->d_qctl, p->qctl_init_v.data(), p->qctl_init_v.size() * sizeof(int),
+                        cudaMemcpyHostToDevice, s);
+  return e;  // (pageable sources are staged before cudaMemcpyAsync returns)
+}
+
+// Rank tables of a partitioned plan: emulated ranks share this process's
+// pools (their replicas sit at the offsets the ops carry); a real rank's
+// own entries are its bound pools, peers' come from hmx_plan_peer.
+cudaError_t upload_peer_tables(hmx_plan* p, cudaStream_t s) {
+  const int R = p->nranks;
+  for (int r = 0; r < R; ++r) {
+    if (p->rank >= 0 && r != p->rank) continue;
+    for (int b = 0; b < 16; ++b) {
+      p->h_r_bases[r * 16 + b] = p->bases[b];
+      p->h_r_rbases[r * 16 + b] = p->rbases[b];
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(p->d_r_bases, p->h_r_bases.data(), R * 16 * sizeof(double*),
+                                  cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMemcpyAsync(p->d_r_rbases, p->h_r_rbases.data(), R * 16 * sizeof(int*),
+                              cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMemcpyAsync(p->d_r_indeg, p->h_r_indeg.data(), R * sizeof(int*), cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMemcpyAsync(p->d_r_queue, p->h_r_queue.data(), R * sizeof(int*), cudaMemcpyHostToDevice, s);
+  if (!e) e = cudaMemcpyAsync(p->d_r_qctl, p->h_r_qctl.data(), R * sizeof(int*), cudaMemcpyHostToDevice, s);
+  return e;
 }
 
 cudaError_t launch_waves(hmx_plan* p, cudaStream_t s) {
@@ -831,6 +951,9 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   }
   p->qctl_init[0] = 0;
   p->qctl_init[1] = r;
+  p->qctl_init_v.assign(p->qctl_init, p->qctl_init + 2);
+  p->indeg_h = indeg;
+  p->wave_tasks_h.assign(d->wave_tasks, d->wave_tasks + nt);
   if (!e) e = upload(&p->d_indeg_init, indeg.data(), (size_t)nt);
   if (!e) e = cudaMalloc(&p->d_indeg, std::max(nt, 1) * sizeof(int));
   if (!e) e = upload(&p->d_queue_init, queue.data(), (size_t)nt);
@@ -905,17 +1028,16 @@ hmx_status hmx_plan_execute(hmx_plan_t p, int32_t mode, void* stream) {
       if (e) return cuda_status(e);
     }
     e = cudaGraphLaunch(p->gexec, s);
-  } else if (mode == 2) {
-    e = cudaMemcpyAsync(p->d_indeg, p->d_indeg_init, p->n_tasks * sizeof(int),
-                        cudaMemcpyDeviceToDevice, s);
-    if (!e) e = cudaMemcpyAsync(p->d_queue, p->d_queue_init, p->n_tasks * sizeof(int),
-                                cudaMemcpyDeviceToDevice, s);
-    if (!e) e = cudaMemcpyAsync(p->d_qctl, p->qctl_init, 2 * sizeof(int), cudaMemcpyHostToDevice, s);
+  } else if (mode == 2 || mode == 4) {
+    if (mode == 2) e = reset_sched(p, s);
+    if (!e && p->nranks > 1) e = upload_peer_tables(p, s);
     if (!e) {
       DevPlan P = make_dev(p);
-      if (p->occ == 2) k_persistent<2><<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
-      else k_persistent<1><<<p->n_ctas, HMX_THREADS, smem, s>>>(P);
-      e = cudaGetLastError();
+      void* args[] = {&P};
+      // cooperative launch: the scheduler's CTAs wait on one another, so
+      // all of them must be resident at once
+      e = cudaLaunchCooperativeKernel(p->occ == 2 ? (const void*)k_persistent<2> : (const void*)k_persistent<1>,
+                                      dim3(p->n_ctas), dim3(HMX_THREADS), args, smem, s);
     }
   } else if (mode == 3) {
     DevPlan P = make_dev(p);
@@ -980,11 +1102,135 @@ hmx_status hmx_plan_destroy(hmx_plan_t p) {
   if (p->gexec) cudaGraphExecDestroy(p->gexec);
   void* ptrs[] = {p->d_ops, p->d_task_ops, p->d_succ_ptr, p->d_succ_idx, p->d_indeg_init,
                   p->d_indeg, p->d_queue_init, p->d_queue, p->d_qctl, p->d_wave_tasks,
-                  p->d_seq_tasks, p->d_scratch, p->d_rscratch, p->d_counters, p->d_status};
+                  p->d_seq_tasks, p->d_scratch, p->d_rscratch, p->d_counters, p->d_status,
+                  p->d_owner, p->d_n_local, p->d_pub_ptr, p->d_pub, p->d_r_bases, p->d_r_rbases,
+                  p->d_r_indeg, p->d_r_queue, p->d_r_qctl};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
   return HMX_OK;
+}
+
+hmx_status hmx_plan_partition(hmx_plan_t p, int32_t nranks, int32_t rank, const int32_t* owner,
+                              const int64_t* pub_ptr, const hmx_pub* pub, int64_t n_pub) {
+  if (!p || nranks < 2 || rank < -1 || rank >= nranks || !owner || !pub_ptr) return HMX_ERR_ARG;
+  if (p->nranks > 1) return HMX_ERR_ARG;  // partition once
+  const int nt = p->n_tasks;
+  for (int t = 0; t < nt; ++t)
+    if (owner[t] < 0 || owner[t] >= nranks) return HMX_ERR_ARG;
+  if (pub_ptr[0] != 0 || pub_ptr[nt] != n_pub) return HMX_ERR_ARG;
+  for (int64_t k = 0; k < n_pub; ++k)
+    if (pub[k].dst < 0 || pub[k].dst >= nranks || pub[k].base < 0 || pub[k].base >= 15 ||
+        pub[k].rbase < 0 || pub[k].rbase >= 15)
+      return HMX_ERR_ARG;
+  p->nranks = nranks;
+  p->rank = rank;
+  // per-rank ready queues (wave order), local task counts
+  std::vector<int> nloc(nranks, 0);
+  for (int t = 0; t < nt; ++t) nloc[owner[t]]++;
+  const int nq = rank < 0 ? nranks : 1;
+  std::vector<int> queue((size_t)nq * nt, -1);
+  p->qctl_init_v.assign(2 * nq, 0);
+  for (int i = 0; i < nt; ++i) {
+    const int t = p->wave_tasks_h[i];
+    if (p->indeg_h[t] != 0) continue;
+    const int r = owner[t];
+    if (rank >= 0 && r != rank) continue;
+    const int qi = rank < 0 ? r : 0;
+    queue[(size_t)qi * nt + p->qctl_init_v[2 * qi + 1]++] = t;
+  }
+  cudaError_t e = cudaSuccess;
+  cudaFree(p->d_queue_init);
+  cudaFree(p->d_queue);
+  cudaFree(p->d_qctl);
+  p->d_queue_init = p->d_queue = p->d_qctl = nullptr;
+  e = upload(&p->d_queue_init, queue.data(), queue.size());
+  if (!e) e = cudaMalloc(&p->d_queue, std::max<size_t>(queue.size(), 1) * sizeof(int));
+  if (!e) e = cudaMalloc(&p->d_qctl, 2 * nq * sizeof(int));
+  if (!e) e = upload(&p->d_owner, owner, (size_t)nt);
+  if (!e) e = upload(&p->d_n_local, nloc.data(), (size_t)nranks);
+  if (!e) e = upload(&p->d_pub_ptr, pub_ptr, (size_t)nt + 1);
+  if (!e) e = upload(&p->d_pub, pub, (size_t)n_pub);
+  p->h_r_bases.assign(16 * nranks, nullptr);
+  p->h_r_rbases.assign(16 * nranks, nullptr);
+  p->h_r_indeg.assign(nranks, nullptr);
+  p->h_r_queue.assign(nranks, nullptr);
+  p->h_r_qctl.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    if (rank >= 0 && r != rank) continue;
+    const int qi = rank < 0 ? r : 0;
+    p->h_r_indeg[r] = p->d_indeg;  // in-degrees are per task: one array serves every emulated rank
+    p->h_r_queue[r] = p->d_queue + (size_t)qi * nt;
+    p->h_r_qctl[r] = p->d_qctl + 2 * qi;
+  }
+  if (!e) e = cudaMalloc(&p->d_r_bases, 16 * nranks * sizeof(double*));
+  if (!e) e = cudaMalloc(&p->d_r_rbases, 16 * nranks * sizeof(int*));
+  if (!e) e = cudaMalloc(&p->d_r_indeg, nranks * sizeof(int*));
+  if (!e) e = cudaMalloc(&p->d_r_queue, nranks * sizeof(int*));
+  if (!e) e = cudaMalloc(&p->d_r_qctl, nranks * sizeof(int*));
+  return cuda_status(e);
+}
+
+hmx_status hmx_plan_sched_state(hmx_plan_t p, void** indeg, void** queue, void** qctl) {
+  if (!p) return HMX_ERR_ARG;
+  if (indeg) *indeg = p->d_indeg;
+  if (queue) *queue = p->d_queue;
+  if (qctl) *qctl = p->d_qctl;
+  return HMX_OK;
+}
+
+hmx_status hmx_plan_peer(hmx_plan_t p, int32_t r, double* const* bases, int32_t* const* rbases,
+                         int32_t* indeg, int32_t* queue, int32_t* qctl) {
+  if (!p || p->nranks < 2 || p->rank < 0 || r < 0 || r >= p->nranks || r == p->rank) return HMX_ERR_ARG;
+  for (int b = 0; b < 16; ++b) {
+    p->h_r_bases[r * 16 + b] = bases ? bases[b] : nullptr;
+    p->h_r_rbases[r * 16 + b] = rbases ? rbases[b] : nullptr;
+  }
+  p->h_r_indeg[r] = indeg;
+  p->h_r_queue[r] = queue;
+  p->h_r_qctl[r] = qctl;
+  return HMX_OK;
+}
+
+hmx_status hmx_plan_reset(hmx_plan_t p, void* stream) {
+  if (!p) return HMX_ERR_ARG;
+  return cuda_status(reset_sched(p, (cudaStream_t)stream));
+}
+
+hmx_status hmx_ipc_handle(const void* dptr, void* handle, int64_t* offset) {
+  if (!dptr || !handle || !offset) return HMX_ERR_ARG;
+  // allocation base through the driver entry point (no link-time libcuda)
+  typedef int (*get_range_t)(unsigned long long*, size_t*, unsigned long long);
+  static get_range_t get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &fn, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess || !fn)
+      return HMX_ERR_CUDA;
+    get_range = (get_range_t)fn;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (unsigned long long)(uintptr_t)dptr) != 0) return HMX_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base);
+  if (e) return cuda_status(e);
+  memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)((uintptr_t)dptr - (uintptr_t)base);
+  return HMX_OK;
+}
+
+hmx_status hmx_ipc_open(const void* handle, void** base) {
+  if (!handle || !base) return HMX_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+hmx_status hmx_ipc_close(void* base) {
+  if (!base) return HMX_ERR_ARG;
+  return cuda_status(cudaIpcCloseMemHandle(base));
 }
 
 hmx_status hmx_fp64_fma_probe(int32_t blocks, int32_t iters, double* out, void* stream) {

@@ -185,6 +185,7 @@ class Planner:
         self.wtop = 0
         self.wslots = 0
         self.nw = 0
+        self.w_info = {}  # micro-task result id -> ([(offset, doubles)], rank slot index or -1)
         self.top = self.peak = 0
         self.peak_task = -1
         self.rtop = self.rpeak = 0
@@ -264,8 +265,11 @@ class Planner:
             W = self._wref(q.m, q.n)
             self.copy(q.m, q.n, 1.0, q.ref, W)
             out = PD(W, q.m, q.n)
+            self.w_info[wid] = ([(W.off, _al(max(q.m * max(q.n, 1), 1)))], -1)
         else:
             Wu, Wv = self._wref(q.m, q.kmax), self._wref(q.n, q.kmax)
+            self.w_info[wid] = ([(Wu.off, _al(max(q.m * max(q.kmax, 1), 1))),
+                                 (Wv.off, _al(max(q.n * max(q.kmax, 1), 1)))], self.wslots)
             ws = self._wslot()
             self.copy(q.m, q.k, 1.0, q.U, Wu)
             self.copy(q.n, q.k, 1.0, q.V, Wv)
@@ -928,6 +932,7 @@ class Planner:
         prog.groups = {newidx[r]: [newidx[t] for t in ms] for r, ms in self.groups.items()}
         prog.ws_size = max(self.wtop, 1)
         prog.ws_slots = max(self.wslots, 1)
+        prog.w_info = dict(self.w_info)
         return prog
 
 
@@ -1011,8 +1016,20 @@ def replicate(prog, nrep, base_sizes, slot_sizes):
     """
     ops = prog.ops
     n = len(ops)
-    out = np.tile(ops, nrep)
-    rep = np.repeat(np.arange(nrep, dtype=np.int64), n)
+    out = shift_ops(np.tile(ops, nrep), np.repeat(np.arange(nrep, dtype=np.int64), n),
+                    base_sizes, slot_sizes)
+    task_ops = prog.task_ops
+    nt = len(task_ops) - 1
+    t_all = (task_ops[None, :-1] + (np.arange(nrep)[:, None] * n)).ravel()
+    new_task_ops = np.concatenate([t_all, [n * nrep]]).astype(np.int64)
+    return out, new_task_ops, nt
+
+
+def shift_ops(out, rep, base_sizes, slot_sizes):
+    """Shift op records ``out`` (in place) to replica ``rep[i]`` of their
+    storage: matrix refs of base b move by rep * base_sizes[b] elements, rank
+    slots of base b by rep * slot_sizes[b]; scratch (base 15) stays."""
+    rep = np.asarray(rep, dtype=np.int64)
     mask56 = (1 << 56) - 1
     for field in ("ref", "wref"):
         r = out[field]
@@ -1038,11 +1055,7 @@ def replicate(prog, nrep, base_sizes, slot_sizes):
             add[sel] = (rep[:, None] * int(sz) * np.ones_like(arr))[sel]
         newcode = (b << 24) | (idx + add)
         arr[neg] = (-(newcode + 1))[neg]
-    task_ops = prog.task_ops
-    nt = len(task_ops) - 1
-    t_all = (task_ops[None, :-1] + (np.arange(nrep)[:, None] * n)).ravel()
-    new_task_ops = np.concatenate([t_all, [n * nrep]]).astype(np.int64)
-    return out, new_task_ops, nt
+    return out
 
 
 OPS = ("hmul", "htrsl", "htrsu", "htrsl_accu", "htrsu_accu")
