@@ -40,7 +40,9 @@ def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_c
 
 
 def clear_plans():
+    """Drop every cached plan (their device scratch is freed with them)."""
     _PLANS.clear()
+    _OPS.clear()
 
 
 def _check_operands(*ms):

@@ -39,3 +39,24 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _release_device_plans(request):
+    """Cached plans hold per-CTA scratch arenas (GBs at c2 size): free them
+    after every GPU test so one module's plans cannot starve the next."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import gc
+
+    from paper_1911_07531_b200 import arith
+
+    arith.clear_plans()
+    gc.collect()
+    try:
+        import torch
+
+        torch.cuda.empty_cache()
+    except Exception:
+        pass

@@ -12,7 +12,7 @@ no dataset).  The problem definitions are restated here independently of the
 product package so that the pin does not depend on the code it pins.
 
 Usage:  python tests/golden/make_golden.py [case ...]
-Cases:  small (s1..s4, trunc), c1, c2, c3s, c4, c5s
+Cases:  small (s1..s4, trunc), c1, c2, c3 (numerics, fast assembly), c3s, c4, c5s
 """
 
 from __future__ import annotations
@@ -67,7 +67,7 @@ def case_points(name):
         g = (np.arange(128) + 0.5) / 128
         X, Y = np.meshgrid(g, g, indexing="ij")
         return np.column_stack([X.ravel(), Y.ravel()]), 0.2, 64, eta_adm(2.0), 1e-6
-    if name == "c3s":
+    if name in ("c3s", "c3"):
         rng = np.random.default_rng(0)
         p = rng.normal(size=(65536, 3))
         p /= np.linalg.norm(p, axis=1, keepdims=True)
@@ -147,8 +147,74 @@ def probe(H, x):
 # case runners
 # ---------------------------------------------------------------------------
 
+def rsvd_lowrank(M, policy, seed):
+    """Large-block compression used only for the c3 fixture (the reference's
+    full-SVD assembly, hmatrix.py:133-138, needs ~1.9e14 flop at c3 and does
+    not finish in a CPU session).  Randomized range finder with one power
+    iteration, sketch doubled until its trailing singular value is below
+    1e-3 of the cut, then the SVD of the projected block and the reference's
+    own ``policy.keep`` (hmatrix.py:62-71) on those singular values.  The
+    same recipe as the device assembly (paper_1911_07531_b200/assembly.py),
+    restated independently; ``check_rsvd_sample`` compares it with the
+    reference's ``dense_to_lowrank`` on a sample of blocks."""
+    m, n = M.shape
+    rng = np.random.default_rng(seed)
+    s = min(m, n, 48)
+    cut = policy.eps
+    while True:
+        G = rng.normal(size=(n, s))
+        Q, _ = np.linalg.qr(M @ G)
+        Q, _ = np.linalg.qr(M @ (M.T @ Q))
+        W, S, Zt = np.linalg.svd(Q.T @ M, full_matrices=False)
+        if S[-1] <= 1e-3 * cut * S[0] or s >= min(m, n):
+            break
+        s = min(min(m, n), 2 * s)
+    r = policy.keep(S)
+    return Q @ (W[:, :r] * S[:r]), Zt[:r].T.copy(), S
+
+
+def assemble_fast(broot, kern, policy, small=128):
+    """hm.assemble with rsvd_lowrank for admissible leaves with min(m,n) >
+    small; smaller admissible leaves use the reference's dense_to_lowrank,
+    dense leaves the reference kernel evaluation (hmatrix.py:227-248)."""
+    A = hm.zeros(broot, policy)
+    nlarge = 0
+    for leaf in A.leaves():
+        b = leaf.block
+        rows = np.arange(b.row.indices.first, b.row.indices.last)
+        cols = np.arange(b.col.indices.first, b.col.indices.last)
+        M = kern.dense(rows, cols)
+        if not b.admissible:
+            leaf.D = np.ascontiguousarray(M, dtype=float)
+        elif min(M.shape) <= small:
+            leaf.set_lowrank(*hm.dense_to_lowrank(M, policy))
+        else:
+            U, V, _ = rsvd_lowrank(M, policy, 777 + b.uid)
+            leaf.set_lowrank(U, V)
+            nlarge += 1
+    return A, nlarge
+
+
+def check_rsvd_sample(broot, kern, policy, count=24, small=128):
+    """Rank of rsvd_lowrank == rank of the reference's dense_to_lowrank on a
+    seeded sample of large admissible blocks (full SVDs, the expensive pin)."""
+    A = hm.zeros(broot, policy)
+    big = [lf.block for lf in A.leaves() if lf.block.admissible
+           and min(lf.block.nrows, lf.block.ncols) > small]
+    pick = np.random.default_rng(5).choice(len(big), size=min(count, len(big)), replace=False)
+    out = []
+    for i in sorted(pick):
+        b = big[i]
+        M = kern.dense(np.arange(b.row.indices.first, b.row.indices.last),
+                       np.arange(b.col.indices.first, b.col.indices.last))
+        U, _ = hm.dense_to_lowrank(M, policy)
+        Ur, _, _ = rsvd_lowrank(M, policy, 777 + b.uid)
+        out.append((int(b.uid), int(M.shape[0]), int(M.shape[1]), int(U.shape[1]), int(Ur.shape[1])))
+    return out
+
+
 def run_case(name, numerics=True, modes=("std", "accu"), dag_modes=None, full_dag=False,
-             store_blocks=True, n_probe=2):
+             store_blocks=True, n_probe=2, fast_assembly=False):
     t0 = time.time()
     pts, ell, n_min, adm, eps = case_points(name)
     geom = trees.Geometry(pts)
@@ -185,7 +251,18 @@ def run_case(name, numerics=True, modes=("std", "accu"), dag_modes=None, full_da
         kern = exp_kernel(pts, ell, perm)
         t1 = time.time()
         hm.counters.reset()
-        A0 = hm.assemble(broot, kern, pol)
+        if fast_assembly:
+            meta["rsvd_vs_reference_sample"] = check_rsvd_sample(broot, kern, pol)
+            print(f"[{name}] rsvd sample {meta['rsvd_vs_reference_sample']}", flush=True)
+            bad = [x for x in meta["rsvd_vs_reference_sample"] if x[3] != x[4]]
+            if bad:
+                raise SystemExit(f"rsvd ranks differ from dense_to_lowrank: {bad}")
+            t1 = time.time()
+            A0, meta["assembly_rsvd_blocks"] = assemble_fast(broot, kern, pol)
+            meta["assembly"] = ("reference kernel evaluation; dense_to_lowrank for admissible "
+                                "min(m,n)<=128, rsvd_lowrank above (make_golden.py)")
+        else:
+            A0 = hm.assemble(broot, kern, pol)
         meta["assembly_truncations"] = hm.counters.snapshot()[0]
         meta["assembly_s"] = time.time() - t1
         print(f"[{name}] assembly {time.time() - t1:.1f}s", flush=True)
@@ -297,6 +374,8 @@ def main(argv):
         elif c == "c3s":
             run_case("c3s", numerics=False, dag_modes=[("std", False), ("accu-merged", False)],
                      store_blocks=False)
+        elif c == "c3":
+            run_case("c3", dag_modes=[], fast_assembly=True)
         elif c == "c4":
             for j in range(4):
                 run_case(f"c4_{j}", dag_modes=[("std", False), ("accu-merged", False)])

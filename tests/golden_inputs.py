@@ -34,7 +34,7 @@ def case(name):
         g = (np.arange(128) + 0.5) / 128
         X, Y = np.meshgrid(g, g, indexing="ij")
         return np.column_stack([X.ravel(), Y.ravel()]), 0.2, 64, "eta", 2.0, 1e-6
-    if name == "c3s":
+    if name in ("c3s", "c3"):
         rng = np.random.default_rng(0)
         p = rng.normal(size=(65536, 3))
         p /= np.linalg.norm(p, axis=1, keepdims=True)
