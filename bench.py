@@ -426,34 +426,32 @@ def main():
             AB0 = H.HBatch.replicate(A0, 1)
             AB = H.HBatch(broot, pol, 1, args.rank_cap)
             LB, UB = H.HBatch(broot, pol, 1, args.rank_cap), H.HBatch(broot, pol, 1, args.rank_cap)
-        hA_v = AB0.store.values.cpu().pin_memory()
-        hA_r = AB0.store.ranks.cpu().pin_memory()
-        hL_v = torch.empty_like(hA_v).pin_memory()
-        hU_v = torch.empty_like(hA_v).pin_memory()
-        hL_r = torch.empty_like(hA_r).pin_memory()
-        hU_r = torch.empty_like(hA_r).pin_memory()
-        e_ms = []
+        # the caller's A in host memory, packed (live leaf data at the actual
+        # ranks, hmatrix.pack_leaves format) in pinned buffers
+        hA_v, hA_r = AB0.download_packed()
+        torch.cuda.synchronize()
+        hA_v, hA_r = hA_v.clone().pin_memory(), hA_r.clone().pin_memory()
+        hL = hU = hLr = hUr = None
+        e_ms, d2h = [], []
         for it in range(args.warmup + args.steps):
             flush.fill_(1.0)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            AB.store.values.copy_(hA_v, non_blocking=True)
-            AB.store.ranks.copy_(hA_r, non_blocking=True)
+            AB.upload_packed(hA_v, hA_r)
             hlu_batch(AB, LB, UB, pol, cfg.mode, exec_mode=em)
-            hL_v.copy_(LB.store.values, non_blocking=True)
-            hU_v.copy_(UB.store.values, non_blocking=True)
-            hL_r.copy_(LB.store.ranks, non_blocking=True)
-            hU_r.copy_(UB.store.ranks, non_blocking=True)
+            hL, hLr = LB.download_packed(hL, hLr)
+            hU, hUr = UB.download_packed(hU, hUr)
             e1.record()
             torch.cuda.synchronize()
             if it >= args.warmup:
                 e_ms.append(e0.elapsed_time(e1))
+                d2h.append((hL.numel() + hU.numel()) * 8 + (hLr.numel() + hUr.numel()) * 4)
         te = max_over_ranks(float(np.mean(e_ms)))
         vb = hA_v.numel() * 8 + hA_r.numel() * 4
         e2e = {"value": world * R * flops / (te * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(vb), "d2h_bytes_per_step": int(2 * vb),
-               "ms_per_step": te, "api": "arith.hlu_batch (hmatrix.HBatch)"}
+               "h2d_bytes_per_step": int(vb), "d2h_bytes_per_step": int(max(d2h)),
+               "ms_per_step": te, "api": "HBatch.upload_packed -> arith.hlu_batch -> HBatch.download_packed (packed live leaf data, pinned host buffers)"}
 
     if rank != 0:
         if dist is not None:

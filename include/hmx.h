@@ -218,6 +218,24 @@ hmx_status hmx_exp_kernel_blocks(int32_t nblocks, const int64_t* desc /* device,
                                  const int64_t* perm, double ell, double diag, double scale,
                                  double* out, void* stream);
 
+/* Packed leaf transfer (wire / dump format).  Replaces the host loops of
+ * HStore.upload_leaves / download_leaves over the reference's per-leaf
+ * numpy arrays (hmatrix.py:141-177: D, or U and V at rank k).  Items are
+ * (instance b < nrep, leaf l < nleaf) in that order; desc (device,
+ * nleaf x 5 int64): uid, off0 (dense block or U offset), off_v (-1 for a
+ * dense leaf), m, n; instance b's pool starts at b*pool_stride and its
+ * rank words at b*rank_stride (indexed by uid).  The packed item is the
+ * dense block (m*n) or U (m*k) then V (n*k), column-major, k = the rank
+ * word.  offsets (device, nleaf*nrep + 1 int64) receives the exclusive scan
+ * of the item sizes (offsets[last] = total doubles).  pack with
+ * packed == NULL only computes offsets. */
+hmx_status hmx_pack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, int64_t pool_stride,
+                           int32_t rank_stride, const double* pool, const int32_t* ranks,
+                           double* packed, int64_t* offsets, void* stream);
+hmx_status hmx_unpack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, int64_t pool_stride,
+                             int32_t rank_stride, const double* packed, const int32_t* ranks,
+                             double* pool, int64_t* offsets, void* stream);
+
 /* FP64 FMA-pipe throughput probe (2*8*iters*256*blocks flops), used by
  * bench.py to measure the FP64 roofline denominator on the box. */
 hmx_status hmx_fp64_fma_probe(int32_t blocks, int32_t iters, double* out, void* stream);

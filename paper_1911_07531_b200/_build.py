@@ -2,7 +2,9 @@
 
 The shared library is the whole device side of the engine: the CTA-level
 fp64 kernels (hmx_device.cuh), the op-program interpreter, the DAG
-executors and the C ABI declared in include/hmx.h.
+executors, the packed leaf transfer kernels and the C ABI declared in
+include/hmx.h.  Each .cu compiles to its own object (rebuilt only when it
+or a header changed), then one link step makes the shared library.
 """
 
 from __future__ import annotations
@@ -15,13 +17,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmx.so")
-SOURCES = ["hmx_engine.cu"]
+SOURCES = ["hmx_engine.cu", "hmx_transfer.cu"]
 HEADERS = ["hmx_device.cuh", os.path.join("..", "..", "include", "hmx.h")]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
 
@@ -33,29 +35,49 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+def _obj(src):
+    return os.path.join(CSRC, os.path.splitext(src)[0] + ".o")
+
+
+def _hdr_time():
+    return max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+
+
+def _obj_stale(src):
+    o = _obj(src)
+    if not os.path.exists(o):
+        return True
+    t = os.path.getmtime(o)
+    return os.path.getmtime(os.path.join(CSRC, src)) > t or _hdr_time() > t
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    for f in SOURCES + HEADERS:
-        if os.path.getmtime(os.path.join(CSRC, f)) > t:
-            return True
-    return False
+    return any(_obj_stale(s) or os.path.getmtime(_obj(s)) > t for s in SOURCES)
+
+
+def _run(cmd, log):
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(log[-1])
+        raise RuntimeError("nvcc failed building libhmx.so")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = res.stdout + res.stderr
+    log = []
+    for s in SOURCES:
+        if force or _obj_stale(s):
+            _run([_nvcc(), *NVCC_FLAGS, "-c", "-o", _obj(s), os.path.join(CSRC, s)], log)
+    _run([_nvcc(), *ARCH, "-shared", "-o", LIB] + [_obj(s) for s in SOURCES], log)
     with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
-        f.write(log)
-    if res.returncode != 0:
-        sys.stderr.write(log)
-        raise RuntimeError("nvcc failed building libhmx.so")
+        f.write("".join(log))
     if verbose:
-        sys.stderr.write(log)
+        sys.stderr.write("".join(log))
     return LIB
 
 

@@ -104,6 +104,8 @@ def lib():
         "hmx_ipc_handle": ([vp, vp, C.POINTER(i64)], i32),
         "hmx_ipc_open": ([vp, C.POINTER(vp)], i32),
         "hmx_ipc_close": ([vp], i32),
+        "hmx_pack_leaves": ([i32, i32, vp, i64, i32, vp, vp, vp, vp, vp], i32),
+        "hmx_unpack_leaves": ([i32, i32, vp, i64, i32, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -122,7 +124,7 @@ EXPORTED = (
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
     "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_plan_trace", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",
     "hmx_plan_partition", "hmx_plan_sched_state", "hmx_plan_peer", "hmx_plan_reset",
-    "hmx_ipc_handle", "hmx_ipc_open", "hmx_ipc_close",
+    "hmx_ipc_handle", "hmx_ipc_open", "hmx_ipc_close", "hmx_pack_leaves", "hmx_unpack_leaves",
 )
 
 

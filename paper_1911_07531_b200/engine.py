@@ -78,6 +78,63 @@ class HStore:
         self.values.copy_(other.values)
         self.ranks.copy_(other.ranks)
 
+    # packed transfers (wire format, csrc/hmx_transfer.cu) -----------------
+    def _pack_desc(self):
+        d = getattr(self.layout, "_pack_desc", None)
+        if d is None:
+            torch = _torch()
+            lay, t = self.layout, self.table
+            rows = []
+            for u in t.leaves(0):
+                if t.adm[u]:
+                    rows.append((u, lay.u_off[u], lay.v_off[u], t.m[u], t.nc[u]))
+                else:
+                    rows.append((u, lay.d_off[u], -1, t.m[u], t.nc[u]))
+            d = torch.from_numpy(np.asarray(rows, dtype=np.int64).reshape(-1, 5)).cuda()
+            self.layout._pack_desc = d
+        return d
+
+    def packed_size(self, stream=None):
+        """Total doubles of the packed form at the current device ranks
+        (one device->host read of the scan total)."""
+        torch = _torch()
+        d = self._pack_desc()
+        nrep = self.nrep
+        offs = torch.empty(d.shape[0] * nrep + 1, dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib().hmx_pack_leaves(d.shape[0], nrep, _lib.ptr(d), self.layout.size,
+                                              self.table.n, None, _lib.ptr(self.ranks), None,
+                                              _lib.ptr(offs), _lib.stream_ptr(stream)), "pack")
+        return int(offs[-1].item())
+
+    def pack_to(self, out, offsets=None, stream=None):
+        """Gather the live leaf data into `out` (device, >= packed_size
+        doubles); returns the device offsets tensor (items + 1)."""
+        torch = _torch()
+        d = self._pack_desc()
+        nrep = self.nrep
+        if offsets is None:
+            offsets = torch.empty(d.shape[0] * nrep + 1, dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib().hmx_pack_leaves(d.shape[0], nrep, _lib.ptr(d), self.layout.size,
+                                              self.table.n, _lib.ptr(self.values),
+                                              _lib.ptr(self.ranks), _lib.ptr(out),
+                                              _lib.ptr(offsets), _lib.stream_ptr(stream)), "pack")
+        return offsets
+
+    def unpack_from(self, packed, offsets=None, stream=None):
+        """Scatter packed leaf data into the pool; self.ranks must already
+        hold the ranks the packed form was made with."""
+        torch = _torch()
+        d = self._pack_desc()
+        nrep = self.nrep
+        if offsets is None:
+            offsets = torch.empty(d.shape[0] * nrep + 1, dtype=torch.int64, device="cuda")
+        _lib.check(_lib.lib().hmx_unpack_leaves(d.shape[0], nrep, _lib.ptr(d), self.layout.size,
+                                                self.table.n, _lib.ptr(packed),
+                                                _lib.ptr(self.ranks), _lib.ptr(self.values),
+                                                _lib.ptr(offsets), _lib.stream_ptr(stream)),
+                   "unpack")
+        return offsets
+
     # host transfers -----------------------------------------------------
     def upload_leaves(self, leaves):
         """leaves: uid -> ("D", M) | ("R", U, V) (row-major numpy)."""

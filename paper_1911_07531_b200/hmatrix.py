@@ -339,3 +339,92 @@ class HBatch:
 
     def copy(self) -> "HBatch":
         return HBatch(self.block, self.policy, self.nrep, store=self.store.clone())
+
+    # packed host transfers (wire / dump format, csrc/hmx_transfer.cu) ------
+    def _xfer_buf(self):
+        import torch
+
+        b = getattr(self, "_xbuf", None)
+        if b is None:
+            b = self._xbuf = torch.empty(self.store.values.numel(), dtype=torch.float64,
+                                         device="cuda")
+        return b
+
+    def upload_packed(self, packed, ranks, stream=None):
+        """Load every member from the packed form: ``packed`` the live leaf
+        data (pack_leaves format, host pinned or device) and ``ranks`` the
+        int32 rank words (nrep x n_blocks).  One H2D copy of each plus one
+        device scatter; nothing of the pools' unused rank capacity moves."""
+        st = self.store
+        if ranks.numel() != st.ranks.numel():
+            raise ValueError("rank words do not match the batch")
+        buf = self._xfer_buf()
+        if packed.numel() > buf.numel():
+            raise ValueError("packed data larger than the batch pools")
+        st.ranks.copy_(ranks, non_blocking=True)
+        buf[:packed.numel()].copy_(packed, non_blocking=True)
+        st.unpack_from(buf, stream=stream)
+
+    def download_packed(self, out=None, out_ranks=None, stream=None):
+        """(packed live data, rank words) of every member on the host (pinned
+        tensors; pass preallocated ones to reuse them)."""
+        import torch
+
+        st = self.store
+        buf = self._xfer_buf()
+        offs = st.pack_to(buf, stream=stream)
+        total = int(offs[-1].item())
+        if out is None or out.numel() < total:
+            out = torch.empty(total, dtype=torch.float64, pin_memory=True)
+        if out_ranks is None:
+            out_ranks = torch.empty(st.ranks.numel(), dtype=torch.int32, pin_memory=True)
+        out[:total].copy_(buf[:total], non_blocking=True)
+        out_ranks.copy_(st.ranks, non_blocking=True)
+        return out[:total], out_ranks
+
+
+def pack_leaves(table: BlockTable, leaves_list, nblocks=None):
+    """Host form of the packed format for a list of members' leaves
+    (uid -> ("D", M) | ("R", U, V), row-major numpy, as download_leaves
+    returns): (packed float64 array, int32 rank words nrep x n_blocks)."""
+    n = table.n
+    parts, ranks = [], []
+    for leaves in leaves_list:
+        r = np.full(n, -1, dtype=np.int32)
+        for u in table.leaves(0):
+            x = leaves[u]
+            if x[0] == "D":
+                parts.append(np.asarray(x[1], dtype=np.float64).T.ravel())
+            else:
+                r[u] = x[1].shape[1]
+                parts.append(np.asarray(x[1], dtype=np.float64).T.ravel())
+                parts.append(np.asarray(x[2], dtype=np.float64).T.ravel())
+        r[table.leaf & table.adm & (r < 0)] = 0
+        ranks.append(r)
+    data = np.concatenate(parts) if parts else np.zeros(0)
+    return data, np.concatenate(ranks)
+
+
+def unpack_leaves(table: BlockTable, packed, ranks, nrep=1):
+    """Inverse of pack_leaves: list of nrep leaf dicts."""
+    packed = np.asarray(packed)
+    ranks = np.asarray(ranks).reshape(nrep, table.n)
+    out, o = [], 0
+    for b in range(nrep):
+        lv = {}
+        for u in table.leaves(0):
+            m, nc = int(table.m[u]), int(table.nc[u])
+            if table.adm[u]:
+                k = int(ranks[b, u])
+                U = packed[o:o + m * k].reshape(k, m).T.copy()
+                o += m * k
+                V = packed[o:o + nc * k].reshape(k, nc).T.copy()
+                o += nc * k
+                lv[u] = ("R", U, V)
+            else:
+                lv[u] = ("D", packed[o:o + m * nc].reshape(nc, m).T.copy())
+                o += m * nc
+        out.append(lv)
+    if o != packed.size:
+        raise ValueError("packed data does not match the rank words")
+    return out

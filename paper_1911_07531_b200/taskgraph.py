@@ -639,6 +639,37 @@ def key_line(k) -> str:
     return f"{kind}|{','.join(map(str, mids))}|{','.join(map(str, uids))}|{alpha!r}"
 
 
+def multiset_digest(node_lines, src, dst):
+    """Order-independent digest of a DAG too large to sort as text (config 5:
+    3.2M nodes, 207M edges).  h = blake2b-64 of each canonical node line;
+    nodes -> (sum h, sum h^2) mod 2^64; edges -> the same two sums over
+    e = h_u * 0x9E3779B97F4A7C15 + (h_v ^ (h_v >> 29)) * 0xBF58476D1CE4E5B9.
+    Same definition as tests/golden/make_golden.py (which ran the reference)."""
+    import hashlib
+
+    h = np.fromiter((int.from_bytes(hashlib.blake2b(x.encode(), digest_size=8).digest(), "little")
+                     for x in node_lines), dtype=np.uint64, count=len(node_lines))
+    with np.errstate(over="ignore"):
+        out = [int(h.sum(dtype=np.uint64)), int((h * h).sum(dtype=np.uint64))]
+        es, ess = np.uint64(0), np.uint64(0)
+        for a in range(0, len(src), 1 << 24):
+            hu, hv = h[src[a:a + (1 << 24)]], h[dst[a:a + (1 << 24)]]
+            e = hu * np.uint64(0x9E3779B97F4A7C15) + (hv ^ (hv >> np.uint64(29))) * np.uint64(0xBF58476D1CE4E5B9)
+            es += e.sum(dtype=np.uint64)
+            ess += (e * e).sum(dtype=np.uint64)
+        out += [int(es), int(ess)]
+    return [f"{x:016x}" for x in out]
+
+
+def dag_digest(g: TaskGraph):
+    """{nodes, edges, digest} of a graph (multiset_digest over its CSR)."""
+    ptr, idx = g.csr()
+    src = np.repeat(np.arange(g.n_nodes, dtype=np.int64), np.diff(ptr.astype(np.int64)))
+    lines = [key_line(t.key()) for t in g.nodes]
+    return {"nodes": g.n_nodes, "edges": int(len(idx)),
+            "digest": multiset_digest(lines, src, idx.astype(np.int64))}
+
+
 def canonical_hashes(g: TaskGraph):
     """sha256 of sorted canonical node and edge lines (fixture format)."""
     import hashlib

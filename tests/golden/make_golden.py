@@ -104,6 +104,37 @@ def sha(text: str) -> str:
     return hashlib.sha256(text.encode()).hexdigest()
 
 
+def multiset_digest(node_lines, src, dst):
+    """Order-independent digest of a DAG for graphs too large to sort as
+    strings (c5: 3.2M nodes, 207M edges): per-node h = blake2b-64 of its
+    canonical line; nodes: (sum h, sum h*h) mod 2^64; edges: the same sums
+    over e = h_u * 0x9E3779B97F4A7C15 + (h_v ^ (h_v >> 29)) * 0xBF58476D1CE4E5B9.
+    Restated in paper_1911_07531_b200/taskgraph.py:multiset_digest."""
+    h = np.fromiter((int.from_bytes(hashlib.blake2b(x.encode(), digest_size=8).digest(), "little")
+                     for x in node_lines), dtype=np.uint64, count=len(node_lines))
+    with np.errstate(over="ignore"):
+        hu, hv = h[src], h[dst]
+        e = hu * np.uint64(0x9E3779B97F4A7C15) + (hv ^ (hv >> np.uint64(29))) * np.uint64(0xBF58476D1CE4E5B9)
+        out = [int(h.sum(dtype=np.uint64)), int((h * h).sum(dtype=np.uint64)),
+               int(e.sum(dtype=np.uint64)), int((e * e).sum(dtype=np.uint64))]
+    return [f"{x:016x}" for x in out]
+
+
+def dag_digest(g):
+    nodes = list(g.nodes)
+    pos = {id(t): i for i, t in enumerate(nodes)}
+    lines = [key_line(t.key()) for t in nodes]
+    ne = sum(1 for _ in g.edges())
+    src = np.empty(ne, dtype=np.int64)
+    dst = np.empty(ne, dtype=np.int64)
+    i = 0
+    for u, v in g.edges():
+        src[i] = pos[id(u)]
+        dst[i] = pos[id(v)]
+        i += 1
+    return {"nodes": len(nodes), "edges": ne, "digest": multiset_digest(lines, src, dst)}
+
+
 def block_table(root):
     rows = []
     for line in trees.serialize_block_tree(root).splitlines():
@@ -379,6 +410,21 @@ def main(argv):
         elif c == "c4":
             for j in range(4):
                 run_case(f"c4_{j}", dag_modes=[("std", False), ("accu-merged", False)])
+        elif c == "c5dag":
+            # reference std DAG of config 5 (478 s, ~17 GB), digest only
+            pts, ell, n_min, adm, eps = case_points("c5s")
+            croot, perm = trees.build_cluster_tree(trees.Geometry(pts), n_min)
+            broot = trees.build_block_tree(croot, croot, adm)
+            out = {}
+            for mode in ("std",):
+                t1 = time.time()
+                g = tg.build_hlu_dag(broot, mode)
+                out[mode] = dag_digest(g)
+                out[mode]["build_s"] = time.time() - t1
+                print(f"[c5dag] {mode} {out[mode]}", flush=True)
+                del g
+            with open(os.path.join(OUT, "c5dag.json"), "w") as f:
+                json.dump(out, f, indent=1, sort_keys=True)
         elif c == "c5s":
             run_case("c5s", numerics=False, dag_modes=[], store_blocks=False)
         else:
