@@ -122,14 +122,15 @@ def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=148):
 
 def main():
     names = {12: "QR", 13: "RRQR", 14: "Jacobi", 15: "recomp"}
-    for (m, n, K) in [(64, 64, 20), (64, 64, 40), (128, 128, 24), (256, 256, 24), (256, 256, 48),
+    shapes = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:] if "," in a]
+    for (m, n, K) in shapes or [(64, 64, 20), (64, 64, 40), (128, 128, 24), (256, 256, 24), (256, 256, 48),
                       (512, 512, 30), (1024, 1024, 30), (1024, 1024, 120), (2048, 2048, 30)]:
         us, st, r, prof = trunc_case(m, n, K, trace=True)
         ph = " ".join(f"{names[c]}={prof[c,0]/max(prof[c,1],1)/1e3:.0f}us" for c in (12, 13, 15))
         sw = prof[14, 1] / max(prof[13, 1], 1)
         print(f"TRUNC m={m:5d} n={n:5d} K={K:4d}: {us:9.1f} us/op  rank~{r:.1f} status={st} "
               f"[{ph} Jacobi={prof[14,0]/max(prof[13,1],1)/1e3:.0f}us sweeps={sw:.1f}]", flush=True)
-    for (m, n) in [(64, 64), (128, 128)]:
+    for (m, n) in ([] if shapes else [(64, 64), (128, 128)]):
         us, st, r = d2lr_case(m, n)
         print(f"D2LR  m={m:5d} n={n:5d}: {us:9.1f} us/op  rank~{r:.1f} status={st}", flush=True)
 
