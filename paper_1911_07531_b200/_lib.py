@@ -12,7 +12,10 @@ import os
 
 import numpy as np
 
-from ._build import LIB
+from ._build import LIB as _BUILT_LIB
+
+# HMX_LIB: load another in-tree build of the same sources (A/B experiments)
+LIB = os.environ.get("HMX_LIB") or _BUILT_LIB
 
 # op codes (hmx_engine.cu)
 OP_NOP, OP_GEMM, OP_COPY, OP_ZERO, OP_ADD, OP_LU, OP_TRSM_LL, OP_TRSM_UT = range(8)

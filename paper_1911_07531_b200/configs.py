@@ -9,6 +9,7 @@ c4  256 independent 1D HODLR instances; instance j: default_rng(1000+j),
     x = sort(uniform(4096)), ell = uniform(0.05, 0.5), leaf 64, eps 1e-6
 c5  262144 points uniform in the unit cube, default_rng(0), ell=0.25,
     leaf 128, eta=2, eps 1e-4, accumulator H-LU
+c5_dD  the first depth-D diagonal sub-problem of c5 (n = 262144 / 2^D)
 
 BASELINE.json leaves the grid convention and the seeds unspecified; the
 choices above are fixed here and in tests/golden/make_golden.py.  Every
@@ -63,6 +64,20 @@ def config(name: str) -> Config:
     if name == "c5":
         rng = np.random.default_rng(0)
         return Config("c5", rng.uniform(size=(262144, 3)), 0.25, 128, "eta", 2.0, 1e-4, "accu")
+    if name.startswith("c5_d"):
+        # the diagonal sub-problem of config 5 at cluster-tree depth d: the
+        # points of the depth-d cluster in tree order.  Splits depend only on
+        # a node's own points (trees.py:104-134; no coordinate ties in a
+        # uniform draw), so its cluster and block trees equal c5's subtree.
+        d = int(name[4:])
+        full = config("c5")
+        _, root, perm, _ = structure(full)
+        node = root
+        for _ in range(d):
+            node = node.children[0]
+        a, b = node.indices.first, node.indices.last
+        return Config(name, full.points[perm[a:b]], full.ell, full.n_min, "eta", full.eta,
+                      full.eps, "accu")
     if name == "s1":
         n = 512
         return Config("s1", ((np.arange(n) + 0.5) / n)[:, None], 0.1, 16, "weak", 0.0, 1e-6, "std")

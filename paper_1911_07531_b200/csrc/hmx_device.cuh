@@ -74,99 +74,220 @@ __device__ void cta_add(int m, int n, double alpha, const double* A, int lda, do
 
 // ---------------------------------------------------------------------------
 // GEMM  C = beta*C + alpha*op(A)*op(B)    (the `@` of hmatrix.py)
-// 64x64 output tiles, k-chunks of 16 staged in shared memory, 4x4 register
-// micro-tile per thread (rows tid%16 + 16i, cols tid/16 + 16j).
-// smem: 2*16*65 doubles.
+// Output tiles of (16*MI) x (16*MJ), MI*MJ = 16: every thread owns an
+// MI x MJ register micro-tile (rows tid%16 + 16i, cols tid/16 + 16j), so
+// the tile shape follows the output shape (64x64 square, 128x32 / 256x16
+// for tall-skinny, 32x128 / 16x256 for short-wide) without idle threads.
+// k-chunks of KC are staged in shared memory and double buffered: the
+// global loads of chunk c+1 are issued into registers before the FMAs of
+// chunk c (one barrier per chunk).  Each output is one thread's fma chain
+// over k in increasing order, so every tile shape gives the same bits.
+// Small outputs with a long reduction (<= 32 4x4 blocks, k >= 128: the
+// V^T C products of blocked Householder) split k over the warps instead
+// (gemm_splitk).  smem: GEMM_SMEM_DOUBLES.
 // ---------------------------------------------------------------------------
 constexpr int GT = 64, GK = 16, GPAD = 65;
 constexpr int GEMM_SMEM_DOUBLES = 4 * GK * GPAD;  // two stages of A and B tiles
 
-// k-chunks are double buffered: the global loads of chunk c+1 are issued
-// into registers before the FMAs of chunk c, so the L2/HBM latency of the
-// operand stream overlaps the arithmetic (one barrier per chunk).
-__device__ void cta_gemm(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
-                         bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
-                         double* C, int ldc, double* sm) {
-  if (m <= 0 || n <= 0) return;
+template <int MI, int MJ, int KC>
+__device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
+                           bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
+                           double* C, int ldc, double* sm) {
+  constexpr int TM = 16 * MI, TN = 16 * MJ, PA = TM + 1, PB = TN + 1;
+  constexpr int SA = KC * PA, SB = KC * PB;
+  static_assert(2 * (SA + SB) <= GEMM_SMEM_DOUBLES, "gemm staging exceeds its smem budget");
+  constexpr int NLA = (TM * KC + HMX_THREADS - 1) / HMX_THREADS;
+  constexpr int NLB = (TN * KC + HMX_THREADS - 1) / HMX_THREADS;
   const int tid = threadIdx.x;
   const int tr = tid & 15, tc = tid >> 4;
-  const int tiles_m = (m + GT - 1) / GT, tiles_n = (n + GT - 1) / GT;
-  constexpr int NL = (GT * GK) / HMX_THREADS;  // elements of each tile per thread
+  const int tiles_m = (m + TM - 1) / TM, tiles_n = (n + TN - 1) / TN;
   for (int tile = 0; tile < tiles_m * tiles_n; ++tile) {
-    const int m0 = (tile % tiles_m) * GT, n0 = (tile / tiles_m) * GT;
-    double acc[4][4];
+    const int m0 = (tile % tiles_m) * TM, n0 = (tile / tiles_m) * TN;
+    double acc[MI][MJ];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    double ra[NL], rb[NL];
+      for (int j = 0; j < MJ; ++j) acc[i][j] = 0.0;
+    double ra[NLA], rb[NLB];
     auto load = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < NL; ++q) {
+      for (int q = 0; q < NLA; ++q) {
         const int e = tid + q * HMX_THREADS;
         int i, kk;
-        if (!ta) { i = e % GT; kk = e / GT; } else { kk = e % GK; i = e / GK; }
+        if (!ta) { i = e % TM; kk = e / TM; } else { kk = e % KC; i = e / KC; }
         const int gi = m0 + i, gk = k0 + kk;
-        ra[q] = (gi < m && gk < k) ? (ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda])
-                                   : 0.0;
+        ra[q] = (e < TM * KC && gi < m && gk < k)
+                    ? (ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda]) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NLB; ++q) {
+        const int e = tid + q * HMX_THREADS;
         int j, kb;
-        if (!tb) { kb = e % GK; j = e / GK; } else { j = e % GT; kb = e / GT; }
+        if (!tb) { kb = e % KC; j = e / KC; } else { j = e % TN; kb = e / TN; }
         const int gj = n0 + j, gkb = k0 + kb;
-        rb[q] = (gj < n && gkb < k) ? (tb ? B[gj + (int64_t)gkb * ldb] : B[gkb + (int64_t)gj * ldb])
-                                    : 0.0;
+        rb[q] = (e < TN * KC && gj < n && gkb < k)
+                    ? (tb ? B[gj + (int64_t)gkb * ldb] : B[gkb + (int64_t)gj * ldb]) : 0.0;
       }
     };
     auto store = [&](int buf) {
-      double* As = sm + buf * 2 * GK * GPAD;
-      double* Bs = As + GK * GPAD;
+      double* As = sm + buf * (SA + SB);
+      double* Bs = As + SA;
 #pragma unroll
-      for (int q = 0; q < NL; ++q) {
+      for (int q = 0; q < NLA; ++q) {
         const int e = tid + q * HMX_THREADS;
         int i, kk;
-        if (!ta) { i = e % GT; kk = e / GT; } else { kk = e % GK; i = e / GK; }
-        As[kk * GPAD + i] = ra[q];
+        if (!ta) { i = e % TM; kk = e / TM; } else { kk = e % KC; i = e / KC; }
+        if (e < TM * KC) As[kk * PA + i] = ra[q];
+      }
+#pragma unroll
+      for (int q = 0; q < NLB; ++q) {
+        const int e = tid + q * HMX_THREADS;
         int j, kb;
-        if (!tb) { kb = e % GK; j = e / GK; } else { j = e % GT; kb = e / GT; }
-        Bs[kb * GPAD + j] = rb[q];
+        if (!tb) { kb = e % KC; j = e / KC; } else { j = e % TN; kb = e / TN; }
+        if (e < TN * KC) Bs[kb * PB + j] = rb[q];
       }
     };
-    const int nk = (k + GK - 1) / GK;
+    const int nk = (k + KC - 1) / KC;
     load(0);
     store(0);
     __syncthreads();
     for (int c = 0; c < nk; ++c) {
-      if (c + 1 < nk) load((c + 1) * GK);
-      const double* As = sm + (c & 1) * 2 * GK * GPAD;
-      const double* Bs = As + GK * GPAD;
-      const int kc = min(GK, k - c * GK);
+      if (c + 1 < nk) load((c + 1) * KC);
+      const double* As = sm + (c & 1) * (SA + SB);
+      const double* Bs = As + SA;
+      const int kc = min(KC, k - c * KC);
       for (int kk = 0; kk < kc; ++kk) {
-        double a[4], b[4];
+        double a[MI], b[MJ];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[kk * GPAD + tr + 16 * i];
+        for (int i = 0; i < MI; ++i) a[i] = As[kk * PA + tr + 16 * i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[kk * GPAD + tc + 16 * j];
+        for (int j = 0; j < MJ; ++j) b[j] = Bs[kk * PB + tc + 16 * j];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < MJ; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
       }
       if (c + 1 < nk) store((c + 1) & 1);
       __syncthreads();
     }
+    // epilogue: all loads of C first (one exposed latency), then the stores
+    if (beta1) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < MJ; ++j) {
+        const int gj = n0 + tc + 16 * j;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int gi = m0 + tr + 16 * i;
+          const double cv = (gi < m && gj < n) ? C[gi + (int64_t)gj * ldc] : 0.0;
+          acc[i][j] = cv + alpha * acc[i][j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < MJ; ++j)
+#pragma unroll
+        for (int i = 0; i < MI; ++i) acc[i][j] = alpha * acc[i][j];
+    }
+#pragma unroll
+    for (int j = 0; j < MJ; ++j) {
       const int gj = n0 + tc + 16 * j;
       if (gj >= n) continue;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < MI; ++i) {
         const int gi = m0 + tr + 16 * i;
-        if (gi >= m) continue;
-        double* cp = C + gi + (int64_t)gj * ldc;
-        *cp = beta1 ? (*cp + alpha * acc[i][j]) : alpha * acc[i][j];
+        if (gi < m) C[gi + (int64_t)gj * ldc] = acc[i][j];
       }
     }
   }
   __syncthreads();
+}
+
+// Split-k GEMM for at most 32 output blocks of 4x4 (lane = block) and a
+// long reduction: warp w sums k in [w*k/8, (w+1)*k/8) for every block, the
+// eight partial tiles meet in shared memory (8 x 32 x 16 doubles).
+__device__ __forceinline__ void gemm_splitk(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
+                            bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
+                            double* C, int ldc, double* sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nbi = (m + 3) >> 2, nbj = (n + 3) >> 2, nblk = nbi * nbj;
+  const int k0 = (int)(((int64_t)k * w) / HMX_WARPS), k1 = (int)(((int64_t)k * (w + 1)) / HMX_WARPS);
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  if (lane < nblk) {
+    const int bi = lane % nbi, bj = lane / nbi;
+    const int i0 = bi * 4, j0 = bj * 4;
+    // element (i, kk) of op(A) at A[ao[i] + kk * as], (kk, j) of op(B) at B[bo[j] + kk * bs]
+    int ao[4], bo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gi = min(i0 + i, m - 1);
+      ao[i] = ta ? gi * lda : gi;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gj = min(j0 + j, n - 1);
+      bo[j] = tb ? gj : gj * ldb;
+    }
+    const int as = ta ? 1 : lda, bs = tb ? ldb : 1;
+#pragma unroll 2
+    for (int kk = k0; kk < k1; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = A[ao[i] + kk * as];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = B[bo[j] + kk * bs];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+  }
+  double* red = sm + (w * 32 + lane) * 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[i * 4 + j] = acc[i][j];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nblk * 16; e += HMX_THREADS) {
+    const int blk = e >> 4, ij = e & 15, i = ij >> 2, j = ij & 3;
+    const int gi = (blk % nbi) * 4 + i, gj = (blk / nbi) * 4 + j;
+    if (gi >= m || gj >= n) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < HMX_WARPS; ++ww) s += sm[(ww * 32 + blk) * 16 + ij];
+    double* cp = C + gi + (int64_t)gj * ldc;
+    *cp = beta1 ? (*cp + alpha * s) : alpha * s;
+  }
+  __syncthreads();
+}
+
+// Inline GEMM of the op interpreter: the 64x64 tile shape only (every
+// extra instantiation raises the register pressure of the whole persistent
+// kernel).
+__device__ __forceinline__ void cta_gemm(int m, int n, int k, double alpha, const double* __restrict__ A,
+                                         int lda, bool ta, const double* __restrict__ B, int ldb, bool tb,
+                                         bool beta1, double* C, int ldc, double* sm) {
+  if (m <= 0 || n <= 0) return;
+  gemm_tiles<4, 4, GK>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+}
+
+// Shape-adaptive GEMM for the large-block paths (blocked QR / Q
+// application, called from __noinline__ functions only).
+__device__ void cta_gemm_wide(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
+                              bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
+                              double* C, int ldc, double* sm) {
+  if (m <= 0 || n <= 0) return;
+  static_assert(HMX_WARPS * 32 * 16 <= GEMM_SMEM_DOUBLES, "split-k partials exceed smem budget");
+  if (k >= 128 && ((m + 3) >> 2) * ((n + 3) >> 2) <= 32) {
+    gemm_splitk(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+    return;
+  }
+  if (n <= 32 && m > 64) gemm_tiles<8, 2, 8>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+  else if (m <= 32 && n > 64) gemm_tiles<2, 8, 8>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+  else gemm_tiles<4, 4, GK>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -722,7 +843,7 @@ __device__ void cta_trmm_small(int jb, int nc, const double* T, bool trans, doub
 
 // ws (global): W (QR_NB x K) + tmp (QR_NB x K).  sm: shared work area of
 // smcap doubles (panel staging + GEMM staging).
-__device__ void cta_qr_blocked(int m, int K, double* A, int lda, double* tau, double* Vx, int ldv,
+__device__ __noinline__ void cta_qr_blocked(int m, int K, double* A, int lda, double* tau, double* Vx, int ldv,
                                double* Tb, double* ws, double* sm, int smcap, double* red) {
   const int p = min(m, K);
   const int nb = qr_nb(m, smcap);
@@ -755,16 +876,16 @@ __device__ void cta_qr_blocked(int m, int K, double* A, int lda, double* tau, do
       double* C = A + j0 + (int64_t)(j0 + jb) * lda;
       double* W = ws;
       double* tmp = ws + (int64_t)QR_NB * K;
-      cta_gemm(jb, nc, rows, 1.0, Vp, ldv, true, C, lda, false, false, W, QR_NB, gsm);
+      cta_gemm_wide(jb, nc, rows, 1.0, Vp, ldv, true, C, lda, false, false, W, QR_NB, gsm);
       cta_trmm_small(jb, nc, T, true, W, QR_NB, tmp);
-      cta_gemm(rows, nc, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, C, lda, gsm);
+      cta_gemm_wide(rows, nc, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, C, lda, gsm);
     }
   }
 }
 
 // X (m x r) := Q X with Q = (I - V0 T0 V0^T)(I - V1 T1 V1^T)...
 // ws: W (QR_NB x r) + tmp (QR_NB x r)
-__device__ void cta_apply_q_blocked(int m, int p, const double* Vx, int ldv, const double* Tb,
+__device__ __noinline__ void cta_apply_q_blocked(int m, int p, const double* Vx, int ldv, const double* Tb,
                                     int r, double* X, int ldx, double* ws, double* gsm,
                                     int smcap) {
   if (r == 0) return;
@@ -777,9 +898,9 @@ __device__ void cta_apply_q_blocked(int m, int p, const double* Vx, int ldv, con
     const double* Vp = Vx + j0 + (int64_t)j0 * ldv;
     const double* T = Tb + (int64_t)b * QR_NB * QR_NB;
     double* Xp = X + j0;
-    cta_gemm(jb, r, rows, 1.0, Vp, ldv, true, Xp, ldx, false, false, W, QR_NB, gsm);
+    cta_gemm_wide(jb, r, rows, 1.0, Vp, ldv, true, Xp, ldx, false, false, W, QR_NB, gsm);
     cta_trmm_small(jb, r, T, false, W, QR_NB, tmp);
-    cta_gemm(rows, r, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, Xp, ldx, gsm);
+    cta_gemm_wide(rows, r, jb, -1.0, Vp, ldv, false, W, QR_NB, false, true, Xp, ldx, gsm);
   }
 }
 

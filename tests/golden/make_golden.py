@@ -81,6 +81,15 @@ def case_points(name):
     if name == "c5s":
         rng = np.random.default_rng(0)
         return rng.uniform(size=(262144, 3)), 0.25, 128, eta_adm(2.0), 1e-4
+    if name.startswith("c5_d"):  # diagonal sub-problem of c5 at depth d (tree order)
+        d = int(name[4:])
+        pts, ell, n_min, adm, eps = case_points("c5s")
+        croot, perm = trees.build_cluster_tree(trees.Geometry(pts), n_min)
+        node = croot
+        for _ in range(d):
+            node = node.children[0]
+        a, b = node.indices.first, node.indices.last
+        return pts[perm[a:b]], ell, n_min, adm, eps
     if name == "s1":  # small 1D HODLR
         n = 512
         return ((np.arange(n) + 0.5) / n)[:, None], 0.1, 16, weak_adm, 1e-6
@@ -407,6 +416,8 @@ def main(argv):
                      store_blocks=False)
         elif c == "c3":
             run_case("c3", dag_modes=[], fast_assembly=True)
+        elif c.startswith("c5_d"):
+            run_case(c, dag_modes=[("accu-merged", False)], modes=("accu",), fast_assembly=True)
         elif c == "c4":
             for j in range(4):
                 run_case(f"c4_{j}", dag_modes=[("std", False), ("accu-merged", False)])

@@ -160,3 +160,33 @@ def test_c5_std_dag_matches_reference():
     d = tg.dag_digest(g)
     assert (d["nodes"], d["edges"]) == (ref["nodes"], ref["edges"])
     assert d["digest"] == ref["digest"]
+
+
+def _rel_blocks(b, a0):
+    out = []
+
+    def rec(x, d):
+        out.append((d, x.row.indices.first - a0, x.row.indices.last - a0, x.col.indices.first - a0,
+                    x.col.indices.last - a0, bool(x.admissible), x.is_leaf))
+        if not x.is_leaf:
+            for row in x.children:
+                for ch in row:
+                    rec(ch, d + 1)
+
+    rec(b, 0)
+    return out
+
+
+@pytest.mark.parametrize("depth", [3])
+def test_c5_subproblem_is_the_diagonal_subtree(depth):
+    """c5_dD (the parity/measurement stand-in for config 5, whose full
+    numerics the CPU reference cannot produce) has exactly the block tree of
+    c5's depth-D diagonal block."""
+    full = configs.config("c5")
+    _, _, _, B = configs.structure(full)
+    node = B
+    for _ in range(depth):
+        node = node.children[0][0]
+    sub = configs.config(f"c5_d{depth}")
+    _, _, _, b = configs.structure(sub)
+    assert _rel_blocks(b, 0) == _rel_blocks(node, node.row.indices.first)
