@@ -132,9 +132,11 @@ def test_reference_fixture_ranks(name):
         assert np.linalg.norm(got - want) <= 10 * eps * np.linalg.norm(want)
 
 
-@pytest.mark.parametrize("name,mode", [("c2", "accu"), ("c2", "std"), ("c3", "accu"), ("c3", "std")])
+@pytest.mark.parametrize("name,mode", [("c2", "accu"), ("c2", "std"), ("c3", "accu"), ("c3", "std"),
+                                       ("c5_d3", "accu")])
 def test_config_ranks_bit_exact_vs_reference(name, mode):
-    """BASELINE configs 2 and 3 end to end on the device: assembly ranks,
+    """BASELINE configs 2, 3 and 5 (its depth-3 diagonal sub-problem, the
+    largest the CPU reference factors in minutes) end to end on the device: assembly ranks,
     every L/U block rank and the truncation/update counters equal the
     unmodified reference's run (tests/golden/c2.*, c3.*); probe products
     within 10*eps, probe residual within 2x of the reference's.  (c3's

@@ -21,7 +21,7 @@ def _sha(s):
     return hashlib.sha256(s.encode()).hexdigest()
 
 
-@pytest.mark.parametrize("name", ["s1", "s2", "s5", "c1", "c2", "c4_0"])
+@pytest.mark.parametrize("name", ["s1", "s2", "s5", "c1", "c2", "c4_0", "c3", "c5_d3"])
 def test_trees_match_reference(name):
     if not have(name):
         pytest.skip("fixture missing")
@@ -127,6 +127,19 @@ def test_c3_dags_match_reference():
     _, _, _, broot = configs.structure(cfg)
     bt = BlockTable(broot)
     for tag, mode in (("std", "std"), ("accu-merged", "accu-merged")):
+        g = tg.build_hlu_dag(bt, mode)
+        ref = meta["dags"][tag]
+        assert g.stats() == (ref["nodes"], ref["edges"])
+        assert tg.canonical_hashes(g) == (ref["nodes_sha"], ref["edges_sha"])
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("HMX_HEAVY"), reason="set HMX_HEAVY=1 (minutes)")
+def test_c5_d3_dag_matches_reference():
+    meta, _ = load("c5_d3")
+    cfg = configs.config("c5_d3")
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    for tag, mode in (("accu-merged", "accu-merged"),):
         g = tg.build_hlu_dag(bt, mode)
         ref = meta["dags"][tag]
         assert g.stats() == (ref["nodes"], ref["edges"])
