@@ -431,27 +431,36 @@ def main():
         hA_v, hA_r = AB0.download_packed()
         torch.cuda.synchronize()
         hA_v, hA_r = hA_v.clone().pin_memory(), hA_r.clone().pin_memory()
-        hL = hU = hLr = hUr = None
-        e_ms, d2h = [], []
-        for it in range(args.warmup + args.steps):
-            flush.fill_(1.0)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            AB.upload_packed(hA_v, hA_r)
-            hlu_batch(AB, LB, UB, pol, cfg.mode, exec_mode=em)
-            hL, hLr = LB.download_packed(hL, hLr)
-            hU, hUr = UB.download_packed(hU, hUr)
-            e1.record()
-            torch.cuda.synchronize()
-            if it >= args.warmup:
-                e_ms.append(e0.elapsed_time(e1))
-                d2h.append((hL.numel() + hU.numel()) * 8 + (hLr.numel() + hUr.numel()) * 4)
-        te = max_over_ranks(float(np.mean(e_ms)))
+        # pipelined host -> device -> host stream of batches (batch.PipelinedHLU):
+        # the H2D of batch i+1 and the D2H of batch i-1 overlap the
+        # factorization of batch i; every batch moves its own packed A in and
+        # its packed L, U (+ rank words) out, all inside the timed region
+        from paper_1911_07531_b200.batch import PipelinedHLU
+
+        del AB, LB, UB
+        torch.cuda.empty_cache()
+        pipe = PipelinedHLU(broot, pol, R, args.rank_cap, cfg.mode, em)
+        inputs = [(hA_v, hA_r)] * max(2, args.warmup)
+        res, ev = pipe.run(inputs)
+        torch.cuda.synchronize()
+        pipe.check()
+        outs = [res[0], res[1]]
+        K = args.steps
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(pipe.s_h2d)
+        res, ev = pipe.run([(hA_v, hA_r)] * K, [outs[i & 1] for i in range(K)])
+        e1.record(pipe.s_d2h)
+        torch.cuda.synchronize()
+        pipe.check()
+        te = max_over_ranks(e0.elapsed_time(e1) / K)
+        (hL, hLr), (hU, hUr) = res[-1]
+        d2h = (hL.numel() + hU.numel()) * 8 + (hLr.numel() + hUr.numel()) * 4
         vb = hA_v.numel() * 8 + hA_r.numel() * 4
         e2e = {"value": world * R * flops / (te * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(vb), "d2h_bytes_per_step": int(max(d2h)),
-               "ms_per_step": te, "api": "HBatch.upload_packed -> arith.hlu_batch -> HBatch.download_packed (packed live leaf data, pinned host buffers)"}
+               "h2d_bytes_per_step": int(vb), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": te, "api": "batch.PipelinedHLU: per step H2D of the packed A batch, unpack, hlu_batch plan, pack, D2H of packed L and U (pinned host buffers); steps pipelined on h2d / compute / d2h streams, K steps in one bracket"}
 
     if rank != 0:
         if dist is not None:

@@ -11,6 +11,14 @@
 
 #ifndef HMX_THREADS
 #define HMX_THREADS 256
+// Numerical stopping parameters of the SVD core (see cta_jacobi_svd and
+// cta_rrqr for the error bounds they imply).
+#ifndef HMX_JACOBI_TOL
+#define HMX_JACOBI_TOL 1e-12
+#endif
+#ifndef HMX_RRQR_THR
+#define HMX_RRQR_THR 1e-5
+#endif
 #endif
 #define HMX_WARPS (HMX_THREADS / 32)
 // 2-D loop over an m x n column-major block without integer division:
@@ -601,7 +609,7 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
   // relative error <= q*tol/2 (relative perturbation of scaled diagonally
   // dominant matrices): q <= 512 gives <= 2.6e-10, far below the rank
   // margins near the cut (>= 4e-5 relative, SURVEY.md finding 4).
-  const double tol = 1e-12;
+  const double tol = HMX_JACOBI_TOL;
   const double tol2 = tol * tol;
   const int npairs = (q + (q & 1)) / 2;
   bool converged = (q <= 1);

@@ -175,7 +175,7 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   double* rest = ws + 6 * q;
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
-  const double thr = sig_out ? 0.0 : 1e-5 * cut;  // see cta_rrqr
+  const double thr = sig_out ? 0.0 : HMX_RRQR_THR * cut;  // see cta_rrqr
   unsigned long long t0 = P.trace ? gtimer2() : 0;
   const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
   phase(P, 13, t0);

@@ -101,3 +101,39 @@ def test_packed_path_factorization_bitwise(mode):
             got = H.unpack_leaves(t, P.numpy(), R.numpy(), 2)
             for b in range(2):
                 _same(got[b], Ref.member(b).store.download_leaves())
+
+
+@pytest.mark.gpu
+def test_pipelined_stream_equals_batched_path():
+    """batch.PipelinedHLU (H2D / factor / D2H overlapped over a stream of
+    batches, two alternating buffer sets) returns per batch exactly the
+    packed factors of the plain hlu_batch path."""
+    import torch
+
+    from paper_1911_07531_b200.arith import hlu_batch
+    from paper_1911_07531_b200.batch import PipelinedHLU
+
+    cfg = configs.config("s2")
+    _, _, perm, broot = configs.structure(cfg)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    t = A.table
+    ins, refs = [], []
+    for scale in (1.0, 0.5, 2.0, 0.25, 4.0):
+        lv = {u: (x[0], *[scale * y for y in x[1:]]) if x[0] == "D" else (x[0], scale * x[1], x[2])
+              for u, x in A.store.download_leaves().items()}
+        data, ranks = H.pack_leaves(t, [lv, lv])
+        ins.append((torch.from_numpy(data).pin_memory(), torch.from_numpy(ranks).pin_memory()))
+        AB, LB, UB = H.HBatch(broot, pol, 2, 64), H.HBatch(broot, pol, 2, 64), H.HBatch(broot, pol, 2, 64)
+        AB.upload_packed(*ins[-1])
+        hlu_batch(AB, LB, UB, pol, "accu")
+        refs.append([M.download_packed() for M in (LB, UB)])
+        torch.cuda.synchronize()
+    pipe = PipelinedHLU(broot, pol, 2, 64, "accu")
+    res, ev = pipe.run(ins)
+    ev.synchronize()
+    pipe.check()
+    for got, want in zip(res, refs):
+        for (gv, gr), (wv, wr) in zip(got, want):
+            assert np.array_equal(gr.numpy(), wr.numpy())
+            assert np.array_equal(gv.numpy(), wv.numpy())
