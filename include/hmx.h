@@ -134,6 +134,14 @@ typedef struct hmx_plan_desc {
   int32_t ctas_per_sm;        /* executor variant: 1 (160 KB shared memory,
                                  255 registers; latency) or 2 (110 KB, 128
                                  registers; batched throughput); 0 = 1     */
+  /* Tiered scratch (optional; NULL / 0 = every CTA gets scratch_doubles).
+   * A task whose need exceeds scratch_doubles runs in one of n_big shared
+   * arenas of big_scratch_doubles, acquired with a device atomic when the
+   * task starts and released when it ends (holders never wait on other
+   * tasks, so acquisition cannot deadlock). */
+  const int64_t* task_scratch; /* host, n_tasks: scratch need per task    */
+  int64_t big_scratch_doubles;
+  int32_t n_big;
 } hmx_plan_desc;
 
 typedef struct hmx_plan* hmx_plan_t;

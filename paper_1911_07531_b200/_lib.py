@@ -62,6 +62,7 @@ class _PlanDesc(C.Structure):
         ("wave_ptr", C.c_void_p), ("wave_tasks", C.c_void_p), ("n_waves", C.c_int32),
         ("scratch_doubles", C.c_int64), ("scratch_ranks", C.c_int32), ("max_ctas", C.c_int32),
         ("ctas_per_sm", C.c_int32),
+        ("task_scratch", C.c_void_p), ("big_scratch_doubles", C.c_int64), ("n_big", C.c_int32),
     ]
 
 
@@ -172,8 +173,24 @@ class Plan:
     """Owning handle of a device execution plan (hmx_plan_t)."""
 
     def __init__(self, ops, task_ops, succ_ptr, succ_idx, wave_ptr, wave_tasks,
-                 scratch_doubles, scratch_ranks, max_ctas=0, ctas_per_sm=1):
+                 scratch_doubles, scratch_ranks, max_ctas=0, ctas_per_sm=1, task_scratch=None,
+                 n_big=0):
+        """task_scratch (per-task need, doubles) enables tiered scratch: each
+        CTA gets a small arena (the 99th percentile of the needs) and tasks
+        above it share n_big (default 16) arenas of the peak size."""
         L = lib()
+        big, ts = 0, None
+        if task_scratch is not None and len(task_scratch):
+            ts = np.ascontiguousarray(task_scratch, dtype=np.int64)
+            peak = int(ts.max())
+            small = max(int(np.percentile(ts, 99)), 1 << 16)
+            if peak > small:
+                scratch_doubles = small
+                big = peak
+                n_big = int(min(int((ts > small).sum()), n_big or 16))
+            else:
+                scratch_doubles = max(peak, 1)
+                n_big = 0
         self._keep = [np.ascontiguousarray(ops, dtype=OP_DTYPE),
                       np.ascontiguousarray(task_ops, dtype=np.int64),
                       np.ascontiguousarray(succ_ptr, dtype=np.int32),
@@ -183,7 +200,9 @@ class Plan:
         o, to, sp, si, wp, wt = self._keep
         d = _PlanDesc(o.ctypes.data, len(o), to.ctypes.data, len(to) - 1, sp.ctypes.data,
                       si.ctypes.data, wp.ctypes.data, wt.ctypes.data, len(wp) - 1,
-                      int(scratch_doubles), int(scratch_ranks), int(max_ctas), int(ctas_per_sm))
+                      int(scratch_doubles), int(scratch_ranks), int(max_ctas), int(ctas_per_sm),
+                      ts.ctypes.data if ts is not None else None, int(big), int(n_big))
+        self.scratch_doubles, self.big_doubles, self.n_big = int(scratch_doubles), int(big), int(n_big)
         h = C.c_void_p()
         check(L.hmx_plan_create(C.byref(d), C.byref(h)), "plan_create")
         self.h = h

@@ -454,16 +454,21 @@ __device__ __forceinline__ int pick_g(int m, int jobs, int nthreads) {
 template <int G>
 __device__ __forceinline__ void grp_apply_reflector(int m, int j, const double* v, double t,
                                                     double* y, int gl, bool active) {
+  // the implicit unit element v_j = 1 belongs to the lane whose first row
+  // is j; it is peeled off so the loops carry no per-element select (same
+  // operations in the same order as the select form: bitwise identical)
   double d = 0.0;
   const int i0 = j + ((gl - j) & (G - 1));
-  if (active) {
+  if (active && i0 < m) {
+    d = (i0 == j) ? y[j] : v[i0] * y[i0];
 #pragma unroll 4
-    for (int i = i0; i < m; i += G) d = fma(i == j ? 1.0 : v[i], y[i], d);
+    for (int i = i0 + G; i < m; i += G) d = fma(v[i], y[i], d);
   }
   d = seg_sum<G>(d) * t;
-  if (active) {
+  if (active && i0 < m) {
+    y[i0] -= (i0 == j) ? d : d * v[i0];
 #pragma unroll 4
-    for (int i = i0; i < m; i += G) y[i] -= d * (i == j ? 1.0 : v[i]);
+    for (int i = i0 + G; i < m; i += G) y[i] -= d * v[i];
   }
 }
 

@@ -86,6 +86,12 @@ struct DevPlan {
   int* const* r_rbases;
   const int64_t* pub_ptr;     // [n_tasks + 1] CSR of the copies a finished task publishes
   const hmx_pub* pub;
+  // tiered scratch: tasks needing more than scratch_stride use a big arena
+  const int64_t* task_need;   // [n_tasks] or null
+  double* big_scratch;
+  int64_t big_stride;
+  int n_big;
+  int* big_lock;              // [n_big] 0 free / 1 held
 };
 
 struct Cx {
@@ -570,11 +576,27 @@ __device__ __forceinline__ unsigned smid() {
 }
 
 __device__ void run_task(const DevPlan& P, int t, double* sm) {
+  __shared__ int s_big;
   unsigned long long t0 = 0;
   if (P.trace && threadIdx.x == 0) t0 = gtimer();
   Cx c;
   c.scratch = P.scratch + (int64_t)blockIdx.x * P.scratch_stride;
   c.rscratch = P.rscratch + (int64_t)blockIdx.x * P.rscratch_stride;
+  const bool big = P.n_big > 0 && P.task_need[t] > P.scratch_stride;
+  if (big) {  // acquire one of the big arenas (holders never block: no deadlock)
+    if (threadIdx.x == 0) {
+      int slot = -1;
+      while (slot < 0) {
+        for (int q = 0; q < P.n_big; ++q)
+          if (atomicCAS(&P.big_lock[q], 0, 1) == 0) { slot = q; break; }
+        if (slot < 0) __nanosleep(200);
+      }
+      __threadfence();
+      s_big = slot;
+    }
+    __syncthreads();
+    c.scratch = P.big_scratch + (int64_t)s_big * P.big_stride;
+  }
   const int64_t b = P.task_ops[t], e = P.task_ops[t + 1];
   for (int64_t i = b; i < e; ++i) {
     const hmx_op o = P.ops[i];
@@ -593,6 +615,13 @@ __device__ void run_task(const DevPlan& P, int t, double* sm) {
       atomicAdd(&prof[2 * (o.code & 15)], dt);
       atomicAdd(&prof[2 * (o.code & 15) + 1], 1ull);
       prof[32 + i] = (dt & ((1ull << 40) - 1)) | (kin << 40);
+    }
+  }
+  if (big) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicExch(&P.big_lock[s_big], 0);
     }
   }
   if (threadIdx.x == 0) {
@@ -790,6 +819,11 @@ struct hmx_plan {
   int max_wave = 0;
   double* d_scratch = nullptr;
   int* d_rscratch = nullptr;
+  int64_t* d_task_need = nullptr;
+  double* d_big = nullptr;
+  int64_t big_stride = 0;
+  int n_big = 0;
+  int* d_big_lock = nullptr;
   int64_t scratch_stride = 0;
   int rscratch_stride = 0;
   int n_ctas = 0;
@@ -862,6 +896,13 @@ DevPlan make_dev(hmx_plan* p) {
     P.pub_ptr = p->d_pub_ptr;
     P.pub = p->d_pub;
   }
+  if (p->n_big > 0) {
+    P.task_need = p->d_task_need;
+    P.big_scratch = p->d_big;
+    P.big_stride = p->big_stride;
+    P.n_big = p->n_big;
+    P.big_lock = p->d_big_lock;
+  }
   return P;
 }
 
@@ -881,6 +922,7 @@ cudaError_t reset_sched(hmx_plan* p, cudaStream_t s) {
   if (!e)
     e = cudaMemcpyAsync(p->d_qctl, p->qctl_init_v.data(), p->qctl_init_v.size() * sizeof(int),
                         cudaMemcpyHostToDevice, s);
+  if (!e && p->d_big_lock) e = cudaMemsetAsync(p->d_big_lock, 0, p->n_big * sizeof(int), s);
   return e;  // (pageable sources are staged before cudaMemcpyAsync returns)
 }
 
@@ -981,6 +1023,18 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   p->rscratch_stride = std::max(d->scratch_ranks, 1);
   if (!e) e = cudaMalloc(&p->d_scratch, (size_t)p->scratch_stride * p->n_ctas * sizeof(double));
   if (!e) e = cudaMalloc(&p->d_rscratch, (size_t)p->rscratch_stride * p->n_ctas * sizeof(int));
+  if (!e && d->task_scratch && d->n_big > 0) {
+    bool any = false;
+    for (int i = 0; i < nt && !any; ++i) any = d->task_scratch[i] > p->scratch_stride;
+    if (any) {
+      p->n_big = d->n_big;
+      p->big_stride = (std::max<int64_t>(d->big_scratch_doubles, p->scratch_stride) + 31) & ~int64_t(31);
+      e = upload(&p->d_task_need, d->task_scratch, (size_t)nt);
+      if (!e) e = cudaMalloc(&p->d_big, (size_t)p->big_stride * p->n_big * sizeof(double));
+      if (!e) e = cudaMalloc(&p->d_big_lock, p->n_big * sizeof(int));
+      if (!e) e = cudaMemset(p->d_big_lock, 0, p->n_big * sizeof(int));
+    }
+  }
   if (!e) e = cudaMalloc(&p->d_counters, 4 * sizeof(unsigned long long));
   if (!e) e = cudaMemset(p->d_counters, 0, 4 * sizeof(unsigned long long));
   if (!e) e = cudaMalloc(&p->d_status, sizeof(int));
@@ -1104,7 +1158,8 @@ hmx_status hmx_plan_destroy(hmx_plan_t p) {
                   p->d_indeg, p->d_queue_init, p->d_queue, p->d_qctl, p->d_wave_tasks,
                   p->d_seq_tasks, p->d_scratch, p->d_rscratch, p->d_counters, p->d_status,
                   p->d_owner, p->d_n_local, p->d_pub_ptr, p->d_pub, p->d_r_bases, p->d_r_rbases,
-                  p->d_r_indeg, p->d_r_queue, p->d_r_qctl};
+                  p->d_r_indeg, p->d_r_queue, p->d_r_qctl, p->d_task_need, p->d_big,
+                  p->d_big_lock};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;

@@ -259,8 +259,10 @@ class ExecPlan:
         # executor variant: one CTA per SM (latency) for a single matrix, two
         # per SM (throughput) for a batch of independent instances
         self.ctas_per_sm = int(ctas_per_sm or (2 if self.nrep > 1 else 1))
+        tsc = prog.task_scratch if self.nrep == 1 else np.tile(prog.task_scratch, self.nrep)
         self.plan = _lib.Plan(ops, task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
-                              prog.scratch_doubles, prog.scratch_ranks, max_ctas, self.ctas_per_sm)
+                              prog.scratch_doubles, prog.scratch_ranks, max_ctas, self.ctas_per_sm,
+                              task_scratch=tsc, n_big=max(16, 2 * self.nrep))
         torch = _torch()
         self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")
@@ -412,7 +414,8 @@ class OpPlan:
         wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.n_tasks = n
         self.plan = _lib.Plan(prog.ops, prog.task_ops, ptr, idx, wave_ptr, order,
-                              prog.scratch_doubles, prog.scratch_ranks, max_ctas)
+                              prog.scratch_doubles, prog.scratch_ranks, max_ctas,
+                              task_scratch=getattr(prog, "task_scratch", None))
         torch = _torch()
         self.acc_values = torch.zeros(prog.acc_size, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1), dtype=torch.int32, device="cuda")

@@ -311,7 +311,8 @@ class PartitionedPlan:
         counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
         wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.plan = _lib.Plan(ops, prog.task_ops, ptr, idx, wave_ptr, order, prog.scratch_doubles,
-                              prog.scratch_ranks, max_ctas, ctas_per_sm)
+                              prog.scratch_ranks, max_ctas, ctas_per_sm,
+                              task_scratch=prog.task_scratch)
         pptr, pub = part.records(self.emulate)
         self.n_pub = len(pub)
         self.plan.partition(self.nranks, self.rank, part.owner, pptr, pub)

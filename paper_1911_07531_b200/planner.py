@@ -188,6 +188,7 @@ class Planner:
         self.w_info = {}  # micro-task result id -> ([(offset, doubles)], rank slot index or -1)
         self.top = self.peak = 0
         self.peak_task = -1
+        self.tpeak = []  # per-task scratch peak (doubles)
         self.rtop = self.rpeak = 0
         self.updates = 0
         # accumulator bookkeeping (accu mode)
@@ -216,6 +217,7 @@ class Planner:
         self.kinds.append(kind)
         self.keys.append(key)
         self.rw.append(([], []))
+        self.tpeak.append(0)
         self.cur = self.task_lists[tid]
         self.cur_id = tid
         self.top = 0
@@ -286,6 +288,8 @@ class Planner:
     def alloc(self, n):
         off = self.top
         self.top += _al(max(int(n), 1))
+        if self.top > self.tpeak[self.cur_id]:
+            self.tpeak[self.cur_id] = self.top
         if self.top > self.peak:
             self.peak = self.top
             self.peak_task = self.cur_id
@@ -925,6 +929,7 @@ class Planner:
         prog.kinds = [self.kinds[t] for t in order]
         prog.fold_chains = {u: [newidx[t] for t in ch] for u, ch in self.fold_chains.items()}
         prog.scratch_doubles = max(self.peak, 1)
+        prog.task_scratch = np.asarray([self.tpeak[t] for t in order], dtype=np.int64)
         prog.scratch_ranks = max(self.rpeak, 1)
         prog.updates = self.updates
         prog.rw = [self.rw[t] for t in order]
@@ -1133,6 +1138,9 @@ def fuse_applies(prog):
     prog.ops = np.concatenate(ops_parts) if ops_parts else prog.ops[:0]
     prog.task_ops = np.asarray(starts + [cur], dtype=np.int64)
     prog.keys, prog.kinds, prog.rw = nkeys, nkinds, nrw
+    # each merged task reuses the scratch from offset 0: its need is the max
+    prog.task_scratch = np.asarray([max(int(prog.task_scratch[t]) for t in grp) for grp in keep],
+                                   dtype=np.int64)
     prog.fold_chains = {u: [merged_into[t] for t in ch] for u, ch in prog.fold_chains.items()}
     prog.groups = {merged_into[r]: [merged_into[t] for t in ms] for r, ms in prog.groups.items()}
     prog.peak_task = merged_into.get(prog.peak_task, -1)

@@ -152,7 +152,8 @@ def test_config_ranks_bit_exact_vs_reference(name, mode):
     cfg = configs.config(name)
     geom, root, perm, broot = configs.structure(cfg)
     pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
-    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    rc = 128 if name.startswith("c5") else 64  # c5 ranks reach 107 (fixture)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=rc)
     rA = A.store.ranks.cpu().numpy()
     sel = arr["A_rank"] >= 0
     assert np.array_equal(rA[sel], arr["A_rank"][sel])
@@ -160,7 +161,7 @@ def test_config_ranks_bit_exact_vs_reference(name, mode):
     bt = O.block_tree(ct, O.adm_standard(ct, cfg.eta))
     X = arr["probe_x"]
     Ax = O.apply(O.HM(bt, A.store.download_leaves()), 0, X)
-    L, U = H.zeros(broot, pol, 64), H.zeros(broot, pol, 64)
+    L, U = H.zeros(broot, pol, rc), H.zeros(broot, pol, rc)
     H.counters.reset()
     if mode == "std":
         hlu(A, L, U, pol)
