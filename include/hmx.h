@@ -141,7 +141,7 @@ typedef struct hmx_plan_desc {
    * tasks, so acquisition cannot deadlock). */
   const int64_t* task_scratch; /* host, n_tasks: scratch need per task    */
   int64_t big_scratch_doubles;
-  int32_t n_big;
+  int32_t n_big;               /* > 0: arenas; < 0: one per -n_big CTAs    */
 } hmx_plan_desc;
 
 typedef struct hmx_plan* hmx_plan_t;

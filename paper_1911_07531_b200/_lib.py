@@ -176,18 +176,20 @@ class Plan:
                  scratch_doubles, scratch_ranks, max_ctas=0, ctas_per_sm=1, task_scratch=None,
                  n_big=0):
         """task_scratch (per-task need, doubles) enables tiered scratch: each
-        CTA gets a small arena (the 99th percentile of the needs) and tasks
-        above it share n_big (default 16) arenas of the peak size."""
+        CTA gets an arena at the 99.9th percentile of the needs; tasks above
+        it share peak-size arenas, one per 4 CTAs (n_big=0) or n_big."""
         L = lib()
         big, ts = 0, None
         if task_scratch is not None and len(task_scratch):
             ts = np.ascontiguousarray(task_scratch, dtype=np.int64)
             peak = int(ts.max())
-            small = max(int(np.percentile(ts, 99)), 1 << 16)
+            small = max(int(np.percentile(ts, 99.9)), 1 << 16)
             if peak > small:
                 scratch_doubles = small
                 big = peak
-                n_big = int(min(int((ts > small).sum()), n_big or 16))
+                n_big = int(n_big) if n_big else -4
+                if n_big > 0:
+                    n_big = int(min(int((ts > small).sum()), n_big))
             else:
                 scratch_doubles = max(peak, 1)
                 n_big = 0

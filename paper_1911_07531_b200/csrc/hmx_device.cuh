@@ -14,10 +14,10 @@
 // Numerical stopping parameters of the SVD core (see cta_jacobi_svd and
 // cta_rrqr for the error bounds they imply).
 #ifndef HMX_JACOBI_TOL
-#define HMX_JACOBI_TOL 1e-12
+#define HMX_JACOBI_TOL 1e-10
 #endif
 #ifndef HMX_RRQR_THR
-#define HMX_RRQR_THR 1e-5
+#define HMX_RRQR_THR 1e-3
 #endif
 #endif
 #define HMX_WARPS (HMX_THREADS / 32)
@@ -612,8 +612,8 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
   // Convergence: |g_a . g_b| <= tol |g_a||g_b| for all pairs.  With
   // G^T G = D^{1/2}(I + F)D^{1/2}, |F_ab| <= tol, every singular value has
   // relative error <= q*tol/2 (relative perturbation of scaled diagonally
-  // dominant matrices): q <= 512 gives <= 2.6e-10, far below the rank
-  // margins near the cut (>= 4e-5 relative, SURVEY.md finding 4).
+  // dominant matrices): tol = 1e-10 and q <= 512 give <= 2.6e-8, far below
+  // the rank margins near the cut (>= 4e-5 relative, SURVEY.md finding 4).
   const double tol = HMX_JACOBI_TOL;
   const double tol2 = tol * tol;
   const int npairs = (q + (q & 1)) / 2;
@@ -661,8 +661,8 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
 // Dropping the trailing rows B = [0 R22] of R is a positive semidefinite
 // change of R^T R = A^T A + B^T B, so every singular value moves by at most
 // ||B||^2 / sigma_i <= thr^2 sigma_1^2 / sigma_i (|R_00| <= sigma_1).  The
-// callers use thr = 1e-5 * cut: singular values at the keep cut
-// (cut * sigma_1) move by <= 1e-10 relative, far below the measured rank
+// callers use thr = HMX_RRQR_THR * cut = 1e-3 * cut: singular values at the
+// keep cut (cut * sigma_1) move by <= thr^2/cut^2 = 1e-6 relative, far below the measured rank
 // margins (>= 4e-5 relative, SURVEY.md finding 4).  Returns k; perm[c] =
 // original column of pivoted column c; tau[j] the reflector scalars; R in
 // rows 0..k-1.

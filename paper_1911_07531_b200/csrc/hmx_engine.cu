@@ -139,7 +139,7 @@ __device__ __forceinline__ double svd_flops(double m, double n) {
 // ---------------------------------------------------------------------------
 // low-rank SVD of a dense p x q block G (destroyed):
 //   rank-revealing QR (stopped once the trailing block is below
-//   1e-5 * cut * sigma_1, see cta_rrqr), then one-sided Jacobi on R1^T
+//   HMX_RRQR_THR * cut * sigma_1, see cta_rrqr), then one-sided Jacobi on R1^T
 //   (QR-preconditioned, so few sweeps), sorted singular values, keep.
 // Writes dstU (p x r) = W_r Sigma_r and dstV (q x r) = Z_r, G ~ dstU dstV^T.
 // ws: >= 6q + 2q^2 doubles.  smw/smcap: shared work area for X and J.
@@ -1023,11 +1023,11 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   p->rscratch_stride = std::max(d->scratch_ranks, 1);
   if (!e) e = cudaMalloc(&p->d_scratch, (size_t)p->scratch_stride * p->n_ctas * sizeof(double));
   if (!e) e = cudaMalloc(&p->d_rscratch, (size_t)p->rscratch_stride * p->n_ctas * sizeof(int));
-  if (!e && d->task_scratch && d->n_big > 0) {
+  if (!e && d->task_scratch && d->n_big != 0) {
     bool any = false;
     for (int i = 0; i < nt && !any; ++i) any = d->task_scratch[i] > p->scratch_stride;
     if (any) {
-      p->n_big = d->n_big;
+      p->n_big = d->n_big > 0 ? d->n_big : std::max(1, p->n_ctas / -d->n_big);
       p->big_stride = (std::max<int64_t>(d->big_scratch_doubles, p->scratch_stride) + 31) & ~int64_t(31);
       e = upload(&p->d_task_need, d->task_scratch, (size_t)nt);
       if (!e) e = cudaMalloc(&p->d_big, (size_t)p->big_stride * p->n_big * sizeof(double));

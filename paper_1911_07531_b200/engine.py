@@ -262,7 +262,7 @@ class ExecPlan:
         tsc = prog.task_scratch if self.nrep == 1 else np.tile(prog.task_scratch, self.nrep)
         self.plan = _lib.Plan(ops, task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
                               prog.scratch_doubles, prog.scratch_ranks, max_ctas, self.ctas_per_sm,
-                              task_scratch=tsc, n_big=max(16, 2 * self.nrep))
+                              task_scratch=tsc)
         torch = _torch()
         self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")

@@ -25,7 +25,7 @@ def _same_leaves(a, b):
 
 @pytest.mark.parametrize("name,mode,nranks", [("s2", "accu", 2), ("s2", "std", 4), ("c1", "std", 2),
                                               ("c1", "accu", 4), ("c2", "accu", 4), ("c2", "std", 8),
-                                              ("c5_d3", "accu", 2)])
+                                              ("c5_d5", "accu", 4)])
 def test_emulated_partition_is_bit_exact(name, mode, nranks):
     from paper_1911_07531_b200 import configs, hmatrix as H
     from paper_1911_07531_b200.arith import run_hlu
