@@ -11,14 +11,14 @@
 
 #ifndef HMX_THREADS
 #define HMX_THREADS 256
+#endif
 // Numerical stopping parameters of the SVD core (see cta_jacobi_svd and
 // cta_rrqr for the error bounds they imply).
 #ifndef HMX_JACOBI_TOL
 #define HMX_JACOBI_TOL 1e-10
 #endif
 #ifndef HMX_RRQR_THR
-#define HMX_RRQR_THR 1e-3
-#endif
+#define HMX_RRQR_THR 1e-4
 #endif
 #define HMX_WARPS (HMX_THREADS / 32)
 // 2-D loop over an m x n column-major block without integer division:
@@ -101,7 +101,8 @@ template <int MI, int MJ, int KC>
 __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, const double* __restrict__ A, int lda,
                            bool ta, const double* __restrict__ B, int ldb, bool tb, bool beta1,
                            double* C, int ldc, double* sm) {
-  constexpr int TM = 16 * MI, TN = 16 * MJ, PA = TM + 1, PB = TN + 1;
+  constexpr int TCOLS = HMX_THREADS / 16;  // thread columns of the 16 x TCOLS grid
+  constexpr int TM = 16 * MI, TN = TCOLS * MJ, PA = TM + 1, PB = TN + 1;
   constexpr int SA = KC * PA, SB = KC * PB;
   static_assert(2 * (SA + SB) <= GEMM_SMEM_DOUBLES, "gemm staging exceeds its smem budget");
   constexpr int NLA = (TM * KC + HMX_THREADS - 1) / HMX_THREADS;
@@ -169,7 +170,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
 #pragma unroll
         for (int i = 0; i < MI; ++i) a[i] = As[kk * PA + tr + 16 * i];
 #pragma unroll
-        for (int j = 0; j < MJ; ++j) b[j] = Bs[kk * PB + tc + 16 * j];
+        for (int j = 0; j < MJ; ++j) b[j] = Bs[kk * PB + tc + TCOLS * j];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -182,7 +183,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
     if (beta1) {
 #pragma unroll
       for (int j = 0; j < MJ; ++j) {
-        const int gj = n0 + tc + 16 * j;
+        const int gj = n0 + tc + TCOLS * j;
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
           const int gi = m0 + tr + 16 * i;
@@ -198,7 +199,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
     }
 #pragma unroll
     for (int j = 0; j < MJ; ++j) {
-      const int gj = n0 + tc + 16 * j;
+      const int gj = n0 + tc + TCOLS * j;
       if (gj >= n) continue;
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
@@ -661,8 +662,9 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
 // Dropping the trailing rows B = [0 R22] of R is a positive semidefinite
 // change of R^T R = A^T A + B^T B, so every singular value moves by at most
 // ||B||^2 / sigma_i <= thr^2 sigma_1^2 / sigma_i (|R_00| <= sigma_1).  The
-// callers use thr = HMX_RRQR_THR * cut = 1e-3 * cut: singular values at the
-// keep cut (cut * sigma_1) move by <= thr^2/cut^2 = 1e-6 relative, far below the measured rank
+// callers use thr = HMX_RRQR_THR * cut = 1e-4 * cut: singular values at the
+// keep cut (cut * sigma_1) move by <= thr^2/cut^2 = 1e-8 relative (1e-3,
+// i.e. 1e-6 relative, flipped one of ~46k block ranks of c3 std), below the measured rank
 // margins (>= 4e-5 relative, SURVEY.md finding 4).  Returns k; perm[c] =
 // original column of pivoted column c; tau[j] the reflector scalars; R in
 // rows 0..k-1.

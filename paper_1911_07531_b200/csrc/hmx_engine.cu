@@ -52,7 +52,12 @@ constexpr int kScratchBase = 15;
 // to 255 registers -- lowest latency per op (single factorizations);
 // 2 CTAs per SM: 110 KB each, registers capped at 128 -- one CTA's
 // barrier/shuffle latency hides behind the other's (batched throughput).
-__host__ __device__ constexpr int smem_doubles(int occ) { return occ == 1 ? 20480 : 14080; }
+// High-occupancy variant: 2 CTAs/SM of 256 threads, or 4 of 128 threads
+// when built with -DHMX_THREADS=128 (experiments).
+constexpr int OCC_HI = HMX_THREADS == 128 ? 4 : 2;
+__host__ __device__ constexpr int smem_doubles(int occ) {
+  return occ == 1 ? 20480 : (occ == 2 ? 14080 : 7040);
+}
 
 struct DevPlan {
   int smem_work;  // usable dynamic shared memory (doubles) of the launched variant
@@ -785,11 +790,11 @@ int num_sms() {
 bool g_attr_set = false;
 cudaError_t set_attrs() {
   if (g_attr_set) return cudaSuccess;
-  const int b1 = smem_doubles(1) * (int)sizeof(double), b2 = smem_doubles(2) * (int)sizeof(double);
+  const int b1 = smem_doubles(1) * (int)sizeof(double), b2 = smem_doubles(OCC_HI) * (int)sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(k_tasks<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b1);
   if (!e) e = cudaFuncSetAttribute(k_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b1);
-  if (!e) e = cudaFuncSetAttribute(k_tasks<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
-  if (!e) e = cudaFuncSetAttribute(k_persistent<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+  if (!e) e = cudaFuncSetAttribute(k_tasks<OCC_HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
+  if (!e) e = cudaFuncSetAttribute(k_persistent<OCC_HI>, cudaFuncAttributeMaxDynamicSharedMemorySize, b2);
   if (e != cudaSuccess) return e;
   g_attr_set = true;
   return cudaSuccess;
@@ -955,7 +960,7 @@ cudaError_t launch_waves(hmx_plan* p, cudaStream_t s) {
     const int b = p->wave_ptr[w], n = p->wave_ptr[w + 1] - b;
     if (!n) continue;
     const int grid = std::min(n, p->n_ctas);
-    if (p->occ == 2) k_tasks<2><<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
+    if (p->occ != 1) k_tasks<OCC_HI><<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
     else k_tasks<1><<<grid, HMX_THREADS, smem, s>>>(P, p->d_wave_tasks + b, n);
   }
   return cudaGetLastError();
@@ -1008,13 +1013,13 @@ hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   std::vector<int> seq(nt);
   for (int i = 0; i < nt; ++i) seq[i] = i;
   if (!e) e = upload(&p->d_seq_tasks, seq.data(), (size_t)nt);
-  p->occ = d->ctas_per_sm == 2 ? 2 : 1;
+  p->occ = d->ctas_per_sm >= 2 ? OCC_HI : 1;
   p->n_ctas = d->max_ctas > 0 ? d->max_ctas : num_sms() * p->occ;
   {  // the persistent scheduler spins: every CTA of its grid must be resident
     int occ = 0;
     const size_t bytes = smem_doubles(p->occ) * sizeof(double);
     const cudaError_t eo =
-        p->occ == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent<2>, HMX_THREADS, bytes)
+        p->occ != 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent<OCC_HI>, HMX_THREADS, bytes)
                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent<1>, HMX_THREADS, bytes);
     if (eo == cudaSuccess && occ > 0) p->n_ctas = std::min(p->n_ctas, occ * num_sms());
   }
@@ -1090,13 +1095,13 @@ hmx_status hmx_plan_execute(hmx_plan_t p, int32_t mode, void* stream) {
       void* args[] = {&P};
       // cooperative launch: the scheduler's CTAs wait on one another, so
       // all of them must be resident at once
-      e = cudaLaunchCooperativeKernel(p->occ == 2 ? (const void*)k_persistent<2> : (const void*)k_persistent<1>,
+      e = cudaLaunchCooperativeKernel(p->occ != 1 ? (const void*)k_persistent<OCC_HI> : (const void*)k_persistent<1>,
                                       dim3(p->n_ctas), dim3(HMX_THREADS), args, smem, s);
     }
   } else if (mode == 3) {
     DevPlan P = make_dev(p);
     for (int t = 0; t < p->n_tasks && !e; ++t) {
-      if (p->occ == 2) k_tasks<2><<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
+      if (p->occ != 1) k_tasks<OCC_HI><<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
       else k_tasks<1><<<1, HMX_THREADS, smem, s>>>(P, p->d_seq_tasks + t, 1);
       e = cudaGetLastError();
     }
