@@ -439,3 +439,37 @@ class OpPlan:
         c = self.plan.counters(stream)
         return {"truncations": c[0], "flops": c[1], "bytes": c[2], "tasks": c[3],
                 "updates": self.prog.updates}
+
+
+class DensePlan:
+    """H x dense operation on one block (planner.plan_dense): apply,
+    apply_t (independent row/column strips, one task each) or the
+    triangular solves (one sequential task).  Bases: 0 = the H-matrix pool,
+    1 = X / Y (column-major, device), 2 = the output of apply / apply_t."""
+
+    def __init__(self, table: BlockTable, op: str, uid: int, cols: int, rank_cap=None):
+        from .planner import plan_dense
+
+        self.table, self.op, self.uid, self.cols = table, op, int(uid), int(cols)
+        prog = plan_dense(table, op, uid, cols, rank_cap)
+        self.prog = prog
+        self.layout = prog.layout
+        n = len(prog.keys)
+        ptr = np.zeros(n + 1, dtype=np.int32)
+        idx = np.zeros(0, dtype=np.int32)
+        self.plan = _lib.Plan(prog.ops, prog.task_ops, ptr, idx, np.array([0, n], np.int32),
+                              np.arange(n, dtype=np.int32), prog.scratch_doubles,
+                              prog.scratch_ranks, task_scratch=prog.task_scratch)
+
+    def run(self, H: HStore, X, out=None, stream=None):
+        if H.layout.table is not self.table:
+            raise ValueError("operand is not over the plan's block tree")
+        self.plan.bind(0, H.values, H.ranks)
+        self.plan.bind(1, X, None)
+        if out is not None:
+            self.plan.bind(2, out, None)
+        self.plan.reset_counters(stream)
+        self.plan.execute(EXEC_PERSISTENT, stream)
+        st = self.plan.status(stream)
+        if st:
+            raise _lib.HmxError(st, self.op)

@@ -428,3 +428,89 @@ def unpack_leaves(table: BlockTable, packed, ranks, nrep=1):
     if o != packed.size:
         raise ValueError("packed data does not match the rank words")
     return out
+
+
+# ---------------------------------------------------------------------------
+# H x dense products and triangular solves (hmatrix.py:286-341) on the device
+# ---------------------------------------------------------------------------
+_DENSE_PLANS = {}
+
+
+def _dense_plan(M: HMatrix, op, cols):
+    from .engine import DensePlan
+
+    t = M.table
+    key = (id(t), op, M.uid, int(cols), M.store.layout.rank_cap)
+    p = _DENSE_PLANS.get(key)
+    if p is None or p.table is not t:
+        p = _DENSE_PLANS[key] = DensePlan(t, op, M.uid, cols, M.store.layout.rank_cap)
+    return p
+
+
+def _dense_run(M: HMatrix, op, X, out_rows):
+    """Run op with X (numpy or torch, rows x cols); returns the same kind."""
+    import torch
+
+    is_np = not isinstance(X, torch.Tensor)
+    Xt = torch.as_tensor(np.asarray(X, dtype=np.float64)) if is_np else X.to(torch.float64)
+    vec = Xt.dim() == 1
+    if vec:
+        Xt = Xt[:, None]
+    cols = int(Xt.shape[1])
+    # column-major device copy (the ops' layout)
+    Xd = Xt.t().contiguous().cuda()
+    if cols == 0:
+        res = torch.zeros(out_rows, 0, dtype=torch.float64)
+    else:
+        p = _dense_plan(M, op, cols)
+        if op in ("apply", "apply_t"):
+            out = torch.empty(out_rows * cols, dtype=torch.float64, device="cuda")
+            p.run(M.store, Xd.view(-1), out)
+            res = out.view(cols, out_rows).t()
+        else:
+            p.run(M.store, Xd.view(-1))
+            res = Xd.view(cols, out_rows).t()
+    if vec:
+        res = res[:, 0]
+    if is_np:
+        return res.cpu().numpy().copy()
+    return res.to(X.device) if X.device.type != "cuda" else res
+
+
+def hm_apply(M: HMatrix, X):
+    """M @ X for a dense X (hmatrix.py:286-299), computed on the device."""
+    if M.ncols != X.shape[0]:
+        raise ValueError("dimension mismatch in apply")
+    return _dense_run(M, "apply", X, M.nrows)
+
+
+def hm_apply_t(M: HMatrix, X):
+    """M.T @ X for a dense X (hmatrix.py:302-315)."""
+    if M.nrows != X.shape[0]:
+        raise ValueError("dimension mismatch in transposed apply")
+    return _dense_run(M, "apply_t", X, M.ncols)
+
+
+def hm_solve_lower(L: HMatrix, Y):
+    """Solve L X = Y, L unit lower triangular, dense Y (hmatrix.py:318-328)."""
+    if L.kind == LOWRANK:
+        raise ValueError("triangular solve on a low-rank diagonal block")
+    if L.nrows != L.ncols or L.nrows != Y.shape[0]:
+        raise ValueError("dimension mismatch in triangular solve")
+    return _dense_run(L, "solve_lower", Y, L.nrows)
+
+
+def hm_solve_upper_t(U: HMatrix, Y):
+    """Solve U.T W = Y, U upper triangular, dense Y (hmatrix.py:331-341)."""
+    if U.kind == LOWRANK:
+        raise ValueError("triangular solve on a low-rank diagonal block")
+    if U.nrows != U.ncols or U.nrows != Y.shape[0]:
+        raise ValueError("dimension mismatch in triangular solve")
+    return _dense_run(U, "solve_upper_t", Y, U.nrows)
+
+
+def lu_residual(A: HMatrix, L: HMatrix, U: HMatrix, X):
+    """||A X - L (U X)||_F / ||A X||_F on the device (probe residual)."""
+    AX = hm_apply(A, X)
+    LUX = hm_apply(L, hm_apply(U, X))
+    return float(np.linalg.norm(np.asarray(AX) - np.asarray(LUX)) / np.linalg.norm(np.asarray(AX)))

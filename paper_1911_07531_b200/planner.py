@@ -1096,6 +1096,100 @@ def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_
     return prog
 
 
+DENSE_OPS = ("apply", "apply_t", "solve_lower", "solve_upper_t")
+
+
+def _elementary(bounds_lo, bounds_hi, lo, hi):
+    """Elementary intervals of [lo, hi) cut at every leaf boundary."""
+    cuts = sorted({lo, hi} | {int(x) for x in bounds_lo} | {int(x) for x in bounds_hi})
+    cuts = [c for c in cuts if lo <= c <= hi]
+    return list(zip(cuts[:-1], cuts[1:]))
+
+
+def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
+    """Program of an H x dense operation on block u (hmatrix.py:286-341).
+
+    apply:         out = H[u] @ X            H=0, X=1 (n_u x cols), out=2 (m_u x cols)
+    apply_t:       out = H[u]^T @ X          X=1 (m_u x cols), out=2 (n_u x cols)
+    solve_lower:   Y := L[u]^{-1} Y          L=0 unit lower, Y=1 (m_u x cols) in place
+    solve_upper_t: Y := U[u]^{-T} Y          U=0 upper, Y=1 in place
+
+    apply / apply_t run one task per elementary row (column) interval of
+    the leaves: each task owns its rows of the output and sums the
+    contributions of the leaves crossing them in block pre-order (a leaf
+    spanning several intervals is applied by row slices, a low-rank one
+    recomputes its small V^T X per slice).  The solves are sequential
+    along the diagonal: one task.
+    """
+    if op not in DENSE_OPS:
+        raise ValueError(op)
+    from .hmatrix import EXACT
+
+    lay = Layout(table, rank_cap)
+    H = PMat(0, lay)
+    p = Planner(EXACT, rank_cap, 0)
+    t = table
+    m_u, n_u = int(t.m[u]), int(t.nc[u])
+    cols = int(cols)
+    if op in ("apply", "apply_t"):
+        tr = op == "apply_t"
+        leaves = list(t.leaves(u))
+        if tr:
+            lo0, hi0 = int(t.c0[u]), int(t.c1[u])
+            ivs = _elementary([t.c0[v] for v in leaves], [t.c1[v] for v in leaves], lo0, hi0)
+        else:
+            lo0, hi0 = int(t.r0[u]), int(t.r1[u])
+            ivs = _elementary([t.r0[v] for v in leaves], [t.r1[v] for v in leaves], lo0, hi0)
+        X = Ref(1, 0, max(n_u if not tr else m_u, 1))
+        O = Ref(2, 0, max(m_u if not tr else n_u, 1))
+        for a, b in ivs:
+            p.begin("dense_" + op, (op, u, a))
+            rows = b - a
+            out = O.at(a - lo0)
+            p.zero(rows, cols, out)
+            for v in leaves:
+                vlo, vhi = (int(t.c0[v]), int(t.c1[v])) if tr else (int(t.r0[v]), int(t.r1[v]))
+                if vhi <= a or vlo >= b:
+                    continue
+                off = a - vlo  # slice of the leaf's rows (apply) / columns (apply_t)
+                if not tr:
+                    c0, nv = int(t.c0[v] - t.c0[u]), int(t.nc[v])
+                    if t.adm[v]:
+                        q = H.lr(v)
+                        mark = p.top
+                        T = p.sref(max(q.kmax, 1), cols)
+                        p.gemm(q.k, cols, nv, 1.0, q.V, True, X.at(c0), False, T, False)
+                        p.gemm(rows, cols, q.k, 1.0, q.U.at(off), False, T, False, out, True)
+                        p.top = mark
+                    else:
+                        p.gemm(rows, cols, nv, 1.0, H.dense(v).at(off), False, X.at(c0), False, out,
+                               True)
+                else:
+                    r0, mv = int(t.r0[v] - t.r0[u]), int(t.m[v])
+                    if t.adm[v]:
+                        q = H.lr(v)
+                        mark = p.top
+                        T = p.sref(max(q.kmax, 1), cols)
+                        p.gemm(q.k, cols, mv, 1.0, q.U, True, X.at(r0), False, T, False)
+                        p.gemm(rows, cols, q.k, 1.0, q.V.at(off), False, T, False, out, True)
+                        p.top = mark
+                    else:
+                        p.gemm(rows, cols, mv, 1.0, H.dense(v).at(0, off), True, X.at(r0), False,
+                               out, True)
+    else:
+        if m_u != n_u:
+            raise ValueError("triangular solve on a non-square block")
+        Y = Ref(1, 0, max(m_u, 1))
+        p.begin("dense_" + op, (op, u))
+        if op == "solve_lower":
+            p.solve_lower(H, u, Y, cols, cols)
+        else:
+            p.solve_upper_t(H, u, Y, cols, cols)
+    prog = p.pack()
+    prog.layout = lay
+    return prog
+
+
 def fuse_applies(prog):
     """Combined accumulator mode: fold every apply_upd task into the leaf
     factor/solve task that follows it in program order (the combined DAG has

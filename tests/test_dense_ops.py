@@ -1,0 +1,77 @@
+"""H x dense operations on the device — hm_apply, hm_apply_t, hm_solve_lower,
+hm_solve_upper_t (hmatrix.py:286-341) — against the oracle restatement of
+the same recursions (oracle/hm_oracle.py apply / apply_t / solve_*), on the
+H-LU factors of the s2 and c1 cases, for the root and for sub-blocks."""
+
+import numpy as np
+import pytest
+
+from oracle import hm_oracle as O
+from paper_1911_07531_b200 import configs, hmatrix as H
+from paper_1911_07531_b200.planner import plan_dense
+
+
+@pytest.mark.parametrize("op", ["apply", "apply_t", "solve_lower", "solve_upper_t"])
+def test_dense_programs_build(op):
+    cfg = configs.config("s2")
+    _, _, _, broot = configs.structure(cfg)
+    t = H.table_of(broot)
+    prog = plan_dense(t, op, 0, 3, 64)
+    n_tasks = len(prog.keys)
+    if op.startswith("apply"):
+        assert n_tasks == len(np.unique(np.concatenate([t.r0[t.leaf], [t.r1[0]]]))) - 1
+    else:
+        assert n_tasks == 1
+    assert prog.task_scratch.shape == (n_tasks,)
+
+
+def _factors(name):
+    from paper_1911_07531_b200.arith import hlu
+
+    cfg = configs.config(name)
+    _, _, perm, broot = configs.structure(cfg)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    A0 = A.copy()
+    L, U = H.zeros(broot, pol, 64), H.zeros(broot, pol, 64)
+    hlu(A, L, U, pol)
+    ct = O.cluster_tree(cfg.points, cfg.n_min)
+    adm = O.adm_weak(ct) if cfg.admissibility == "weak" else O.adm_standard(ct, cfg.eta)
+    bt = O.block_tree(ct, adm)
+    return cfg, bt, A0, L, U
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["s2", "c1"])
+def test_dense_ops_match_oracle(name):
+    cfg, bt, A, L, U = _factors(name)
+    Ah = O.HM(bt, A.store.download_leaves())
+    Lh = O.HM(bt, L.store.download_leaves())
+    Uh = O.HM(bt, U.store.download_leaves())
+    rng = np.random.default_rng(3)
+    n = cfg.n
+    X = rng.normal(size=(n, 3))
+    tol = 1e-12
+    for M, Mh in ((A, Ah), (L, Lh), (U, Uh)):
+        for uid in (0, int(bt.kids[0][1]), int(bt.kids[0][2])):
+            V = H.HMatrix(M.store, uid)
+            m, nc = V.nrows, V.ncols
+            got = H.hm_apply(V, X[:nc])
+            want = O.apply(Mh, uid, X[:nc])
+            assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
+            got = H.hm_apply_t(V, X[:m])
+            want = O.apply_t(Mh, uid, X[:m])
+            assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
+    for uid in (0, int(bt.kids[0][0])):
+        m = H.HMatrix(L.store, uid).nrows
+        got = H.hm_solve_lower(H.HMatrix(L.store, uid), X[:m])
+        want = O.solve_lower(Lh, uid, X[:m])
+        assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want)
+        got = H.hm_solve_upper_t(H.HMatrix(U.store, uid), X[:m])
+        want = O.solve_upper_t(Uh, uid, X[:m])
+        assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+    # vector right-hand side and the device probe residual
+    y = H.hm_apply(A, X[:, 0])
+    assert y.shape == (n,)
+    res = H.lu_residual(A, L, U, X)
+    assert res <= 100 * cfg.eps
