@@ -391,10 +391,11 @@ class OpPlan:
     DAGs, taskgraph.py:146-180); the execution graph comes from the data
     flow of the sequential recursion."""
 
-    def __init__(self, table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, max_ctas=0):
+    def __init__(self, table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, max_ctas=0,
+                 uids=None):
         self.table = table
         self.op = op
-        prog = plan_op(table, op, policy, rank_cap, alpha=alpha)
+        prog = plan_op(table, op, policy, rank_cap, alpha=alpha, uids=uids)
         self.prog = prog
         self.layout = prog.layout
         tables = {b: table for b in range(4)}

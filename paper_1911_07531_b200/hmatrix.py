@@ -514,3 +514,35 @@ def lu_residual(A: HMatrix, L: HMatrix, U: HMatrix, X):
     AX = hm_apply(A, X)
     LUX = hm_apply(L, hm_apply(U, X))
     return float(np.linalg.norm(np.asarray(AX) - np.asarray(LUX)) / np.linalg.norm(np.asarray(AX)))
+
+
+_LEAF_UPD = {}
+
+
+def leaf_update(C: HMatrix, alpha: float, A: HMatrix, B: HMatrix, policy: TruncationPolicy):
+    """C += alpha * A @ B where C is a leaf, A and B of any kind
+    (hmatrix.py:451-460: product_payload then fold_payload_into_leaf), as a
+    one-task device program; A, B, C may live in different H-matrices over
+    the same block tree."""
+    from .engine import OpPlan
+
+    if alpha == 0.0:
+        return
+    if A.nrows != C.nrows or B.ncols != C.ncols or A.ncols != B.nrows:
+        raise ValueError("non-conformal leaf update")
+    if C.kind == BLOCKED:
+        raise ValueError("leaf_update needs a leaf C")
+    t = C.table
+    if A.table is not t or B.table is not t:
+        raise ValueError("operands over different block trees")
+    if C.store is A.store or C.store is B.store:
+        raise ValueError("the output may not alias an input")
+    rc = C.store.layout.rank_cap
+    key = (id(t), A.uid, B.uid, C.uid, float(alpha), repr(policy), rc)
+    p = _LEAF_UPD.get(key)
+    if p is None or p.table is not t:
+        p = _LEAF_UPD[key] = OpPlan(t, "leaf_update", policy, rc, alpha=alpha,
+                                    uids=(A.uid, B.uid, C.uid))
+    p.run(A.store, B.store, C.store)
+    c = p.counters()
+    counters.add(c["truncations"], c["updates"])

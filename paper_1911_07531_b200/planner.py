@@ -1063,23 +1063,31 @@ def shift_ops(out, rep, base_sizes, slot_sizes):
     return out
 
 
-OPS = ("hmul", "htrsl", "htrsu", "htrsl_accu", "htrsu_accu")
+OPS = ("hmul", "htrsl", "htrsu", "htrsl_accu", "htrsu_accu", "leaf_update")
 
 
-def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_min=0):
+def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_min=0,
+            uids=None):
     """Program of a standalone multiply / triangular solve over ``table``.
 
     hmul:  C += alpha A B          (arith.py:40-55)      A=0, B=1, C=2
     htrsl: L X = M, M consumed     (arith.py:97-117)     L=0, M=1, X=2
     htrsu: X U = M, M consumed     (arith.py:120-140)    U=0, M=1, X=2
     *_accu: the accumulator variants (accumulator.py:190-235), acc=3
+    leaf_update: C[uc] += alpha A[ua] B[ub], C[uc] a leaf (hmatrix.py:451-460)
     """
     if op not in OPS:
         raise ValueError(op)
     lay = Layout(table, rank_cap)
     P0, P1, P2 = PMat(0, lay), PMat(1, lay), PMat(2, lay)
     p = Planner(policy, rank_cap, split_min)
-    if op == "hmul":
+    if op == "leaf_update":
+        ua, ub, uc = (int(x) for x in uids)
+        if not table.leaf[uc]:
+            raise ValueError("leaf_update needs a leaf C")
+        p.begin("leaf_update", ("leaf_update", (ua, ub, uc), alpha))
+        p.scatter(P2, uc, p.product(alpha, P0, ua, P1, ub))
+    elif op == "hmul":
         p.hmul(alpha, P0, 0, P1, 0, P2, 0)
     elif op == "htrsl":
         p.htrsl(P0, 0, P1, 0, P2)

@@ -75,3 +75,37 @@ def test_dense_ops_match_oracle(name):
     assert y.shape == (n,)
     res = H.lu_residual(A, L, U, X)
     assert res <= 100 * cfg.eps
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["s2", "c1"])
+def test_leaf_update_matches_oracle(name):
+    """hmatrix.leaf_update (hmatrix.py:451-460): C[(t,s)] += -1 * L[(t,t)] @
+    U[(t,s)] for admissible leaves (t,s) (blocked times low-rank into a
+    low-rank leaf) and C starting at zero: rank and entries equal the
+    oracle's product + fold within 1e-12 relative."""
+    cfg, bt, A, L, U = _factors(name)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    Lh = O.HM(bt, L.store.download_leaves())
+    Uh = O.HM(bt, U.store.download_leaves())
+    opol = O.Policy("accuracy", eps=cfg.eps)
+    C = H.zeros(A.block, pol, 64)
+    Ch = O.HM(bt, C.store.download_leaves())
+    n_b = len(bt.r0)
+    diag = {(int(bt.r0[v]), int(bt.r1[v])): v for v in range(n_b)
+            if bt.r0[v] == bt.c0[v] and bt.r1[v] == bt.c1[v]}
+    done = 0
+    for uc in bt.leaves(0):
+        if not bt.adm[uc] or done >= 3:
+            continue
+        ua = diag[(int(bt.r0[uc]), int(bt.r1[uc]))]
+        H.leaf_update(H.HMatrix(C.store, uc), -1.0, H.HMatrix(L.store, ua),
+                      H.HMatrix(U.store, uc), pol)
+        O.fold_leaf(Ch, uc, O.product(-1.0, Lh, ua, Uh, uc, opol), opol)
+        got, want = C.store.download_leaf(uc), Ch.lv[uc]
+        assert got[0] == want[0] == "R"
+        assert got[1].shape == want[1].shape
+        G, W = got[1] @ got[2].T, want[1] @ want[2].T
+        assert np.linalg.norm(G - W) <= 1e-12 * max(np.linalg.norm(W), 1e-300)
+        done += 1
+    assert done > 0
