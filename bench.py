@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """H-LU benchmark on B200 (BASELINE.json metric, config c2 by default).
 
-One step = R (default 8) independent accumulator H-LU factorizations of the
+One step = R (default 16) independent accumulator H-LU factorizations of the
 config-2 matrix (2D 128x128 grid, exp kernel ell=0.2, eta=2, eps=1e-6,
 leaf 64; n=16384) executed in ONE persistent-scheduler launch over the
 replicated lowered program; the latency of a single factorization (R=1) is
@@ -314,7 +314,7 @@ def main():
     ap.add_argument("--instances", type=int, default=256, help="config 4 batch size (total)")
     ap.add_argument("--ctas-per-sm", type=int, default=0,
                     help="executor variant for the batched run (0 = auto: 2 when replicas > 1)")
-    ap.add_argument("--replicas", type=int, default=8,
+    ap.add_argument("--replicas", type=int, default=16,
                     help="independent factorizations per GPU per step (throughput)")
     args = ap.parse_args()
     if args.impl == "reference":
