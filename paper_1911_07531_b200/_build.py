@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmx.so")
+DAG_LIB = os.path.join(HERE, "libhmxdag.so")  # host C++: native DAG builder (hmx_dag.cpp)
 SOURCES = ["hmx_engine.cu", "hmx_transfer.cu"]
 HEADERS = ["hmx_device.cuh", os.path.join("..", "..", "include", "hmx.h")]
 
@@ -66,7 +67,20 @@ def _run(cmd, log):
         raise RuntimeError("nvcc failed building libhmx.so")
 
 
+def build_dag(force: bool = False) -> str:
+    """g++ -O2 -shared: the host-side refinement DAG builder."""
+    src = os.path.join(CSRC, "hmx_dag.cpp")
+    if force or not os.path.exists(DAG_LIB) or os.path.getmtime(src) > os.path.getmtime(DAG_LIB):
+        res = subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall", "-o", DAG_LIB,
+                              src], capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("g++ failed building libhmxdag.so")
+    return DAG_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_dag(force)
     if not force and not _stale():
         return LIB
     log = []

@@ -678,3 +678,130 @@ def canonical_hashes(g: TaskGraph):
     edges = sorted(f"{key_line(u.key())}>{key_line(v.key())}" for u, v in g.edges())
     h = lambda s: hashlib.sha256("\n".join(s).encode()).hexdigest()  # noqa: E731
     return h(nodes), h(edges)
+
+
+# ---------------------------------------------------------------------------
+# native builder (csrc/hmx_dag.cpp, libhmxdag.so): same node and edge sets
+# ---------------------------------------------------------------------------
+_KIND_NAMES = (HLU, HTRSL, HTRSU, HMUL, ADD_UPD, SHIFT_UPD, APPLY_UPD, LEAF_FACTOR, LEAF_SOLVE_L,
+               LEAF_SOLVE_U, LEAF_UPDATE)
+_MODE_CODE = {STD: 0, COMBINED: 1, MERGED: 2}
+_OP_CODE = {"hlu": 0, "hmul": 1, "htrsl": 2, "htrsu": 3}
+_dag_lib = None
+
+
+def _native():
+    global _dag_lib
+    if _dag_lib is None:
+        import ctypes as C
+
+        from ._build import DAG_LIB
+
+        L = C.CDLL(DAG_LIB)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.hmx_dag_build.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, i64, i32, C.POINTER(vp)]
+        L.hmx_dag_build.restype = C.c_int
+        L.hmx_dag_nodes.argtypes = [vp]
+        L.hmx_dag_nodes.restype = i64
+        L.hmx_dag_edges.argtypes = [vp]
+        L.hmx_dag_edges.restype = i64
+        L.hmx_dag_export.argtypes = [vp] * 9
+        L.hmx_dag_export.restype = C.c_int
+        L.hmx_dag_free.argtypes = [vp]
+        L.hmx_dag_free.restype = None
+        _dag_lib = L
+    return _dag_lib
+
+
+class NativeTask:
+    """Read-only task of a NativeTaskGraph (same key() as Task)."""
+
+    __slots__ = ("kind", "mids", "uids", "alpha", "_g", "_i")
+
+    def __init__(self, g, i, kind, mids, uids, alpha):
+        self.kind, self.mids, self.uids, self.alpha, self._g, self._i = kind, mids, uids, alpha, g, i
+
+    def key(self):
+        return (self.kind, self.mids, self.uids, self.alpha)
+
+    @property
+    def succ(self):
+        g = self._g
+        return [g.nodes[j] for j in g.succ_idx[g.succ_ptr[self._i]:g.succ_ptr[self._i + 1]]]
+
+    def __repr__(self):
+        return f"NativeTask({self.kind}, {self.uids})"
+
+
+class NativeTaskGraph:
+    """DAG from the native builder: node arrays in creation-sequence order
+    (the order of TaskGraph.nodes) and successor CSR."""
+
+    def __init__(self, kind, nm, mids, nu, uids, alpha, ptr, idx, mode, table):
+        self.mode, self.table = mode, table
+        self.succ_ptr, self.succ_idx = ptr, idx
+        self.nodes = [NativeTask(self, i, _KIND_NAMES[kind[i]], tuple(int(x) for x in mids[i, :nm[i]]),
+                                 tuple(int(x) for x in uids[i, :nu[i]]), float(alpha[i]))
+                      for i in range(len(kind))]
+
+    @property
+    def n_nodes(self):
+        return len(self.nodes)
+
+    @property
+    def n_edges(self):
+        return int(len(self.succ_idx))
+
+    def stats(self):
+        return self.n_nodes, self.n_edges
+
+    def edges(self):
+        ptr, idx, nodes = self.succ_ptr, self.succ_idx, self.nodes
+        for i in range(len(nodes)):
+            for j in idx[ptr[i]:ptr[i + 1]]:
+                yield nodes[i], nodes[j]
+
+    def csr(self):
+        return self.succ_ptr.astype(np.int32), self.succ_idx.astype(np.int32)
+
+    def levels(self, extra_edges=None):
+        return asap_levels(len(self.nodes), *self.csr(), extra_edges)
+
+
+def build_dag_native(block_root, mode: str = STD, *, stop_size: int = 0, op: str = "hlu"):
+    """Native (C++) refinement build; same node and edge sets as
+    build_hlu_dag / compute_dag without sparsification."""
+    import ctypes as C
+
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    t = _as_table(block_root)
+    L = _native()
+    arr = [np.ascontiguousarray(x, dtype=np.int64) for x in (t.r0, t.r1, t.c0, t.c1)]
+    leaf = np.ascontiguousarray(t.leaf, dtype=np.int8)
+    parent = np.ascontiguousarray(t.parent, dtype=np.int32)
+    kids = np.ascontiguousarray(np.where(t.kids < 0, -1, t.kids), dtype=np.int32).reshape(-1, 4)
+    h = C.c_void_p()
+    rc = L.hmx_dag_build(t.n, *[a.ctypes.data for a in arr], leaf.ctypes.data, parent.ctypes.data,
+                         kids.ctypes.data, _MODE_CODE[mode], int(stop_size), _OP_CODE[op], C.byref(h))
+    if rc == 2:
+        raise ValueError("structural error in refinement (leaf diagonal / operands)")
+    if rc == 3:
+        raise CycleError("refinement produced a cyclic graph")
+    if rc:
+        raise ValueError(f"hmx_dag_build failed ({rc})")
+    try:
+        n, ne = L.hmx_dag_nodes(h), L.hmx_dag_edges(h)
+        kind = np.empty(n, np.int32)
+        nm = np.empty(n, np.int32)
+        nu = np.empty(n, np.int32)
+        mids = np.empty((n, 3), np.int32)
+        uids = np.empty((n, 3), np.int32)
+        alpha = np.empty(n, np.float64)
+        ptr = np.empty(n + 1, np.int64)
+        idx = np.empty(max(ne, 1), np.int32)
+        L.hmx_dag_export(h, kind.ctypes.data, nm.ctypes.data, mids.ctypes.data, nu.ctypes.data,
+                         uids.ctypes.data, alpha.ctypes.data, ptr.ctypes.data, idx.ctypes.data)
+    finally:
+        L.hmx_dag_free(h)
+    return NativeTaskGraph(kind, nm, mids, nu, uids, alpha, ptr, idx[:ne], mode, t)
