@@ -236,10 +236,12 @@ hmx_status hmx_exp_kernel_blocks(int32_t nblocks, const int64_t* desc /* device,
  * dense block (m*n) or U (m*k) then V (n*k), column-major, k = the rank
  * word.  offsets (device, nleaf*nrep + 1 int64) receives the exclusive scan
  * of the item sizes (offsets[last] = total doubles).  pack with
- * packed == NULL only computes offsets. */
+ * packed == NULL only computes offsets; pack writes at most `capacity`
+ * doubles (items that would end beyond it are skipped: the caller sees
+ * offsets[last] > capacity and packs again into a larger buffer). */
 hmx_status hmx_pack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, int64_t pool_stride,
                            int32_t rank_stride, const double* pool, const int32_t* ranks,
-                           double* packed, int64_t* offsets, void* stream);
+                           double* packed, int64_t capacity, int64_t* offsets, void* stream);
 hmx_status hmx_unpack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, int64_t pool_stride,
                              int32_t rank_stride, const double* packed, const int32_t* ranks,
                              double* pool, int64_t* offsets, void* stream);

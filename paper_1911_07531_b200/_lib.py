@@ -108,7 +108,7 @@ def lib():
         "hmx_ipc_handle": ([vp, vp, C.POINTER(i64)], i32),
         "hmx_ipc_open": ([vp, C.POINTER(vp)], i32),
         "hmx_ipc_close": ([vp], i32),
-        "hmx_pack_leaves": ([i32, i32, vp, i64, i32, vp, vp, vp, vp, vp], i32),
+        "hmx_pack_leaves": ([i32, i32, vp, i64, i32, vp, vp, vp, i64, vp, vp], i32),
         "hmx_unpack_leaves": ([i32, i32, vp, i64, i32, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

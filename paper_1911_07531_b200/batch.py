@@ -119,6 +119,9 @@ class PipelinedHLU:
 
         b = i & 1
         A, L, U = self.sets[b]
+        if A._xfer_buf().numel() < packed.numel():  # first use: size the staging buffer
+            torch.cuda.synchronize()
+            A._xfer_buf(packed.numel())
         buf = A._xfer_buf()
         with torch.cuda.stream(self.s_h2d):
             if self.ev_out[b] is not None:  # A's staging buffer is free once batch i-2 ran
@@ -151,6 +154,10 @@ class PipelinedHLU:
         with torch.cuda.stream(self.s_d2h):
             for k, M in enumerate((L, U)):
                 n = int(self.size_host[b][k])
+                if n > M._xfer_buf().numel():  # packed form outgrew the buffer: grow, pack again
+                    torch.cuda.synchronize()
+                    M._xfer_buf(n)
+                    M.store.pack_to(M._xfer_buf(), self.offs[b][k], stream=self.s_d2h)
                 hv, hr = out[k] if out is not None else (None, None)
                 if hv is None or hv.numel() < n:
                     hv = torch.empty(n, dtype=torch.float64, pin_memory=True)

@@ -373,6 +373,63 @@ __device__ void cta_trsm_upper_trans(int n, int c, const double* T, int ldt, dou
   }
 }
 
+// Warp-per-column-group triangular solve for n <= 128 (no block barriers):
+// T is the factor staged so that the multiplier of row i at pivot l is
+// T[i + l*ldt] (L itself for the unit-lower solve, U^T for the transposed
+// upper solve).  Lane owns rows lane + 32q; a warp solves up to 4 columns of
+// B at once, keeping them in registers; the pivot value travels by shuffle.
+// Every element sees the same operations in the same order as the
+// CTA-wide sweeps above (bitwise-identical results).
+template <bool UNIT>
+__device__ void warp_trsm_cols(int n, int c, const double* T, int ldt, double* B, int ldb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int j0 = w * 4; j0 < c; j0 += HMX_WARPS * 4) {
+    const int nc = min(4, c - j0);
+    double b[4][4];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        b[cc][q] = (cc < nc && i < n) ? B[i + (int64_t)(j0 + cc) * ldb] : 0.0;
+      }
+    for (int l = 0; l < n; ++l) {
+      const int ql = l >> 5, ll = l & 31;
+      double x[4];
+      if (!UNIT) {
+        const double d = T[l + (int64_t)l * ldt];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == ql && lane == ll) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) b[cc][q] /= d;
+          }
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const double v = ql == 0 ? b[cc][0] : ql == 1 ? b[cc][1] : ql == 2 ? b[cc][2] : b[cc][3];
+        x[cc] = __shfl_sync(0xffffffffu, v, ll);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        if (i > l && i < n) {
+          const double t = T[i + (int64_t)l * ldt];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) b[cc][q] -= t * x[cc];
+        }
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        if (cc < nc && i < n) B[i + (int64_t)(j0 + cc) * ldb] = b[cc][q];
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Householder QR (LAPACK dgeqr2 / dlarfg convention), in place on the
 // m x K matrix A: R in the upper triangle, reflectors v (v0 = 1 implicit)

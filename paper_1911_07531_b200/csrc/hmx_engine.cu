@@ -505,6 +505,18 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       double* B = mref(P, c, o.ref[2]);
       int ldb = o.ld[2];
       double* Ts = work;
+      if (n <= 128 && n * n <= P.smem_work) {
+        // multipliers staged as T[i + l n] (U transposed for the upper solve),
+        // then one warp per group of columns, no block barriers
+        if (o.code == OP_TRSM_LL) FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];
+        else FOR_MN(i, j, n, n) Ts[i + j * n] = T[j + (int64_t)i * ldt];
+        __syncthreads();
+        if (o.code == OP_TRSM_LL) warp_trsm_cols<true>(n, cc, Ts, n, B, ldb);
+        else warp_trsm_cols<false>(n, cc, Ts, n, B, ldb);
+        __syncthreads();
+        count(P, (double)n * n * cc, 8.0 * ((double)n * n / 2.0 + 2.0 * n * cc));
+        break;
+      }
       const bool stageT = n * n <= P.smem_work;
       if (stageT) {
         FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];

@@ -79,16 +79,20 @@ __device__ __forceinline__ void seg_copy(const double* __restrict__ src, double*
 }
 
 // pack: pool -> packed (dir = 0); unpack: packed -> pool (dir = 1)
+// pack items that would end beyond `capacity` doubles are skipped (the
+// caller sees offsets[nitems] > capacity, grows its buffer and packs again)
 __global__ void __launch_bounds__(256) k_move(int32_t nleaf, int32_t nrep, const int64_t* desc,
                                               int64_t pool_stride, int32_t rank_stride,
                                               const int32_t* ranks, const int64_t* offsets,
-                                              double* pool, double* packed, int dir) {
+                                              double* pool, double* packed, int dir,
+                                              int64_t capacity) {
   const int64_t nitems = (int64_t)nleaf * nrep;
   for (int64_t i = blockIdx.x; i < nitems; i += gridDim.x) {
     const int64_t b = i / nleaf, l = i - b * nleaf;
     const int64_t* d = desc + 5 * l;
     const int64_t m = d[3], n = d[4];
     double* base = pool + b * pool_stride;
+    if (dir == 0 && offsets[i + 1] > capacity) continue;
     double* pk = packed + offsets[i];
     if (d[2] < 0) {
       if (dir == 0) seg_copy(base + d[1], pk, m * n);
@@ -123,14 +127,14 @@ extern "C" {
 
 hmx_status hmx_pack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, int64_t pool_stride,
                            int32_t rank_stride, const double* pool, const int32_t* ranks,
-                           double* packed, int64_t* offsets, void* stream) {
+                           double* packed, int64_t capacity, int64_t* offsets, void* stream) {
   if (nleaf < 0 || nrep < 0 || !desc || !ranks || !offsets) return HMX_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   k_scan_sizes<<<1, kScanThreads, 0, s>>>(nleaf, nrep, desc, rank_stride, ranks, offsets);
   if (packed && pool && (int64_t)nleaf * nrep > 0)
     k_move<<<grid_for((int64_t)nleaf * nrep), 256, 0, s>>>(nleaf, nrep, desc, pool_stride, rank_stride,
                                                           ranks, offsets, const_cast<double*>(pool),
-                                                          packed, 0);
+                                                          packed, 0, capacity);
   return status_of(cudaGetLastError());
 }
 
@@ -143,7 +147,7 @@ hmx_status hmx_unpack_leaves(int32_t nleaf, int32_t nrep, const int64_t* desc, i
   if ((int64_t)nleaf * nrep > 0)
     k_move<<<grid_for((int64_t)nleaf * nrep), 256, 0, s>>>(nleaf, nrep, desc, pool_stride, rank_stride,
                                                           ranks, offsets, pool,
-                                                          const_cast<double*>(packed), 1);
+                                                          const_cast<double*>(packed), 1, INT64_MAX);
   return status_of(cudaGetLastError());
 }
 

@@ -102,13 +102,14 @@ class HStore:
         nrep = self.nrep
         offs = torch.empty(d.shape[0] * nrep + 1, dtype=torch.int64, device="cuda")
         _lib.check(_lib.lib().hmx_pack_leaves(d.shape[0], nrep, _lib.ptr(d), self.layout.size,
-                                              self.table.n, None, _lib.ptr(self.ranks), None,
+                                              self.table.n, None, _lib.ptr(self.ranks), None, 0,
                                               _lib.ptr(offs), _lib.stream_ptr(stream)), "pack")
         return int(offs[-1].item())
 
     def pack_to(self, out, offsets=None, stream=None):
-        """Gather the live leaf data into `out` (device, >= packed_size
-        doubles); returns the device offsets tensor (items + 1)."""
+        """Gather the live leaf data into `out` (device; items beyond its
+        length are skipped, see hmx_pack_leaves); returns the device offsets
+        tensor (items + 1), whose last entry is the packed size."""
         torch = _torch()
         d = self._pack_desc()
         nrep = self.nrep
@@ -116,7 +117,7 @@ class HStore:
             offsets = torch.empty(d.shape[0] * nrep + 1, dtype=torch.int64, device="cuda")
         _lib.check(_lib.lib().hmx_pack_leaves(d.shape[0], nrep, _lib.ptr(d), self.layout.size,
                                               self.table.n, _lib.ptr(self.values),
-                                              _lib.ptr(self.ranks), _lib.ptr(out),
+                                              _lib.ptr(self.ranks), _lib.ptr(out), out.numel(),
                                               _lib.ptr(offsets), _lib.stream_ptr(stream)), "pack")
         return offsets
 

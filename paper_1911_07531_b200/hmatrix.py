@@ -341,13 +341,14 @@ class HBatch:
         return HBatch(self.block, self.policy, self.nrep, store=self.store.clone())
 
     # packed host transfers (wire / dump format, csrc/hmx_transfer.cu) ------
-    def _xfer_buf(self):
+    def _xfer_buf(self, n=0):
+        """Device staging buffer of the packed form, grown to >= n doubles."""
         import torch
 
         b = getattr(self, "_xbuf", None)
-        if b is None:
-            b = self._xbuf = torch.empty(self.store.values.numel(), dtype=torch.float64,
-                                         device="cuda")
+        if b is None or b.numel() < n:
+            self._xbuf = None
+            b = self._xbuf = torch.empty(max(int(n), 1), dtype=torch.float64, device="cuda")
         return b
 
     def upload_packed(self, packed, ranks, stream=None):
@@ -358,9 +359,9 @@ class HBatch:
         st = self.store
         if ranks.numel() != st.ranks.numel():
             raise ValueError("rank words do not match the batch")
-        buf = self._xfer_buf()
-        if packed.numel() > buf.numel():
+        if packed.numel() > st.values.numel():
             raise ValueError("packed data larger than the batch pools")
+        buf = self._xfer_buf(packed.numel())
         st.ranks.copy_(ranks, non_blocking=True)
         buf[:packed.numel()].copy_(packed, non_blocking=True)
         st.unpack_from(buf, stream=stream)
@@ -374,6 +375,9 @@ class HBatch:
         buf = self._xfer_buf()
         offs = st.pack_to(buf, stream=stream)
         total = int(offs[-1].item())
+        if total > buf.numel():  # grow and pack again
+            buf = self._xfer_buf(total)
+            offs = st.pack_to(buf, offs, stream=stream)
         if out is None or out.numel() < total:
             out = torch.empty(total, dtype=torch.float64, pin_memory=True)
         if out_ranks is None:
