@@ -4,6 +4,5 @@ O=gpurun_out
 for v in "$@"; do
   lib=paper_1911_07531_b200/libhmx${v}.so
   HMX_LIB=$PWD/$lib timeout 900 python bench.py --steps 3 --no-cpu-baseline --no-e2e $BENCH_ARGS > $O/ab2_bench${v}.log 2>&1
-  HMX_LIB=$PWD/$lib timeout 300 python -m pytest tests/test_hlu_gpu.py -q -x -k "oracle" > $O/ab2_pt${v}.log 2>&1
+  HMX_LIB=$PWD/$lib timeout 900 python -m pytest tests/test_hlu_gpu.py -q -x -k "oracle or config_ranks" > $O/ab2_pt${v}.log 2>&1
 done
-HMX_LIB=$PWD/paper_1911_07531_b200/libhmx.so timeout 900 python bench.py --steps 3 --no-cpu-baseline --no-e2e --replicas 16 > $O/ab2_bench_r16.log 2>&1
