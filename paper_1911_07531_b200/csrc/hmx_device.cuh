@@ -544,25 +544,16 @@ __device__ __forceinline__ void grp_update_cols(int m, int j, const double* x, d
   }
 }
 
-// One barrier per step (look-ahead): column j+1 is updated by the first lane
-// group, which sits in warp 0, so warp 0 builds reflector j+1 right after its
-// share of the step-j update while the other warps finish theirs.  Each
-// column sees the same operations in the same order as the two-barrier form.
 __device__ void qr_steps(int m, int K, double* A, int lda, double* tau, int wbeg, int nw, int bar) {
   const int p = min(m, K);
   const int w = (int)(threadIdx.x >> 5) - wbeg;
-  if (p <= 0) return;
-  if (w == 0) warp_reflector(m, 0, A, tau);
-  if (bar) named_bar(bar, nw * 32); else __syncthreads();
   for (int j = 0; j < p; ++j) {
     double* x = A + (int64_t)j * lda;
+    if (w == 0) warp_reflector(m, j, x, tau);
+    if (bar) named_bar(bar, nw * 32); else __syncthreads();
     const double t = tau[j];
     if (t != 0.0)  // ~8 rows per lane (measured best for the step-synchronous QR)
       HMX_G_DISPATCH(m, (grp_update_cols<GG>(m, j, x, t, A, lda, j + 1, K, wbeg * 32, nw * 32)));
-    if (w == 0 && j + 1 < p) {
-      __syncwarp();
-      warp_reflector(m, j + 1, A + (int64_t)(j + 1) * lda, tau);
-    }
     if (bar) named_bar(bar, nw * 32); else __syncthreads();
   }
 }
