@@ -42,6 +42,10 @@ WORKLOADS = {
           "leaf 64, standard H-LU, instances sharded across GPUs",
     "c2": "c2: 2D grid 128x128, exp kernel ell=0.2, eta=2, eps=1e-6, leaf 64, n=16384, accumulator H-LU",
     "c1": "c1: 1D HODLR n=2048, exp kernel ell=0.1, eps=1e-6, leaf 64, standard H-LU",
+    "c3": "c3: 65536 points on the unit sphere, exp kernel ell=0.3, eta=2, eps=1e-5, leaf 64, "
+          "accumulator H-LU",
+    "c5_d3": "c5_d3: depth-3 diagonal sub-problem of c5 (n=32768 of 262144 points in the unit cube), "
+             "exp kernel ell=0.25, eta=2, eps=1e-4, leaf 128, accumulator H-LU",
 }
 
 
