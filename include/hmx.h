@@ -81,6 +81,14 @@ hmx_status hmx_trsm_upper_trans_batched(int32_t batch, int32_t n, int32_t c, con
                                         int32_t ldu, int64_t strideU, double* B, int32_t ldb,
                                         int64_t strideB, void* stream);
 
+/* Back substitution on a dense leaf, B := U^{-1} B (U upper, non-unit):
+ * the leaf step of the solve phase with the factors (hm_solve_upper,
+ * the non-transposed counterpart of hmatrix.py:331-341).
+ * No reference entry point: the reference stops at the factorization. */
+hmx_status hmx_trsm_upper_batched(int32_t batch, int32_t n, int32_t c, const double* U,
+                                  int32_t ldu, int64_t strideU, double* B, int32_t ldb,
+                                  int64_t strideB, void* stream);
+
 /* The `@` products of hmatrix.py (dense leaf GEMM, LR apply, expansion):
  * C = beta*C + alpha*op(A)*op(B); trans flags 0/1. */
 hmx_status hmx_gemm_batched(int32_t batch, int32_t m, int32_t n, int32_t k, double alpha,

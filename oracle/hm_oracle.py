@@ -383,6 +383,24 @@ def solve_lower(L, u, Y):
     return np.vstack([X0, X1])
 
 
+def solve_upper(U, u, Y):
+    """Back substitution U X = Y over the block tree: the non-transposed
+    counterpart of hm_solve_upper_t (hmatrix.py:331-341) for the solve
+    phase (no reference entry point; checked by the residual in tests)."""
+    bt = U.bt
+    if bt.leaf(u):
+        x = U.lv[u]
+        if x[0] != "D":
+            raise ValueError("triangular solve on a low-rank diagonal block")
+        COUNT.flops += float(x[1].shape[0]) ** 2 * Y.shape[1]
+        return sla.solve_triangular(x[1], Y, lower=False)
+    k00, k01, _, k11 = bt.kids[u]
+    n0 = bt.shape(k00)[0]
+    X1 = solve_upper(U, k11, Y[n0:])
+    X0 = solve_upper(U, k00, Y[:n0] - apply(U, k01, X1))
+    return np.vstack([X0, X1])
+
+
 def solve_upper_t(U, u, Y):
     """hm_solve_upper_t (hmatrix.py:331-341)."""
     bt = U.bt

@@ -19,7 +19,7 @@ LIB = os.environ.get("HMX_LIB") or _BUILT_LIB
 
 # op codes (hmx_engine.cu)
 OP_NOP, OP_GEMM, OP_COPY, OP_ZERO, OP_ADD, OP_LU, OP_TRSM_LL, OP_TRSM_UT = range(8)
-OP_TRUNC, OP_D2LR, OP_SETRANK, OP_APPEND, OP_SVALS = 8, 9, 10, 11, 12
+OP_TRUNC, OP_D2LR, OP_SETRANK, OP_APPEND, OP_SVALS, OP_TRSM_UN = 8, 9, 10, 11, 12, 13
 F_TA, F_TB, F_ACC = 1, 2, 4
 SCRATCH_BASE = 15
 
@@ -84,6 +84,7 @@ def lib():
         "hmx_getrf_nopiv_batched": ([i32, i32, vp, i32, i64, vp, vp, i64, vp, vp], i32),
         "hmx_trsm_lower_unit_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
         "hmx_trsm_upper_trans_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
+        "hmx_trsm_upper_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
         "hmx_gemm_batched": ([i32, i32, i32, i32, f64, vp, i32, i64, i32, vp, i32, i64, i32, f64,
                               vp, i32, i64, vp], i32),
         "hmx_truncate_batched": ([i32, i32, i32, i32, vp, vp, i64, i64, i32, i32, f64, i32, vp, vp,
@@ -123,7 +124,7 @@ def lib():
 
 EXPORTED = (
     "hmx_version", "hmx_op_size", "hmx_getrf_nopiv_batched", "hmx_trsm_lower_unit_batched",
-    "hmx_trsm_upper_trans_batched", "hmx_gemm_batched", "hmx_truncate_batched",
+    "hmx_trsm_upper_trans_batched", "hmx_trsm_upper_batched", "hmx_gemm_batched", "hmx_truncate_batched",
     "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",
     "hmx_plan_reset_counters", "hmx_plan_destroy", "hmx_plan_trace", "hmx_exp_kernel_blocks", "hmx_fp64_fma_probe",

@@ -17,6 +17,9 @@
 #ifndef HMX_JACOBI_TOL
 #define HMX_JACOBI_TOL 1e-10
 #endif
+#ifndef HMX_JROT
+#define HMX_JROT 0
+#endif
 #ifndef HMX_RRQR_THR
 #define HMX_RRQR_THR 1e-4
 #endif
@@ -373,14 +376,32 @@ __device__ void cta_trsm_upper_trans(int n, int c, const double* T, int ldt, dou
   }
 }
 
+// Back substitution B := U^{-1} B (U upper, non-unit; the solve phase
+// with the factors, hm_solve_upper below hm_solve_lower):
+// pivots l = n-1 .. 0, divide row l, then eliminate it from rows 0..l-1.
+__device__ void cta_trsm_upper(int n, int c, const double* T, int ldt, double* B, int ldb) {
+  for (int l = n - 1; l >= 0; --l) {
+    const double d = T[l + (int64_t)l * ldt];
+    for (int j = threadIdx.x; j < c; j += HMX_THREADS) B[l + (int64_t)j * ldb] /= d;
+    __syncthreads();
+    for (int e = threadIdx.x; e < l * c; e += HMX_THREADS) {
+      const int i = e % l, j = e / l;
+      B[i + (int64_t)j * ldb] -= T[i + (int64_t)l * ldt] * B[l + (int64_t)j * ldb];
+    }
+    __syncthreads();
+  }
+}
+
 // Warp-per-column-group triangular solve for n <= 128 (no block barriers):
 // T is the factor staged so that the multiplier of row i at pivot l is
 // T[i + l*ldt] (L itself for the unit-lower solve, U^T for the transposed
 // upper solve).  Lane owns rows lane + 32q; a warp solves up to 4 columns of
 // B at once, keeping them in registers; the pivot value travels by shuffle.
 // Every element sees the same operations in the same order as the
-// CTA-wide sweeps above (bitwise-identical results).
-template <bool UNIT>
+// CTA-wide sweeps above (bitwise-identical results).  REV addresses the
+// rows of B in reverse (row n-1-i), which turns the back substitution of
+// an upper solve into this forward sweep (T staged reversed by the caller).
+template <bool UNIT, bool REV = false>
 __device__ void warp_trsm_cols(int n, int c, const double* T, int ldt, double* B, int ldb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int j0 = w * 4; j0 < c; j0 += HMX_WARPS * 4) {
@@ -391,7 +412,7 @@ __device__ void warp_trsm_cols(int n, int c, const double* T, int ldt, double* B
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = lane + 32 * q;
-        b[cc][q] = (cc < nc && i < n) ? B[i + (int64_t)(j0 + cc) * ldb] : 0.0;
+        b[cc][q] = (cc < nc && i < n) ? B[(REV ? n - 1 - i : i) + (int64_t)(j0 + cc) * ldb] : 0.0;
       }
     for (int l = 0; l < n; ++l) {
       const int ql = l >> 5, ll = l & 31;
@@ -425,7 +446,7 @@ __device__ void warp_trsm_cols(int n, int c, const double* T, int ldt, double* B
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int i = lane + 32 * q;
-        if (cc < nc && i < n) B[i + (int64_t)(j0 + cc) * ldb] = b[cc][q];
+        if (cc < nc && i < n) B[(REV ? n - 1 - i : i) + (int64_t)(j0 + cc) * ldb] = b[cc][q];
       }
   }
 }
@@ -642,9 +663,22 @@ __device__ void jacobi_rounds(int p, int q, double* Gm, int ldg, double* J, int 
       }
       al = seg_sum<G>(al); be = seg_sum<G>(be); ga = seg_sum<G>(ga);
       if (!valid || al == 0.0 || be == 0.0 || ga * ga <= tol2 * al * be) continue;
+#if HMX_JROT
+      // the same rotation from two reciprocal square roots (no fp64 divide
+      // or sqrt on the round's critical path): with d = be - al, g = 2 ga,
+      // h = |(d, g)|, cos 2theta = |d|/h, c = sqrt((1 + cos 2theta)/2),
+      // s = sign(d) g / (2 c h); c^2 + s^2 = 1 exactly in exact arithmetic
+      const double d = be - al, g2 = 2.0 * ga;
+      const double rh = rsqrt(fma(d, d, g2 * g2));
+      const double hc = fma(0.5 * fabs(d), rh, 0.5);  // c^2, in [1/2, 1]
+      const double rc = rsqrt(hc);
+      const double c = hc * rc;
+      const double s = copysign(0.5, d) * g2 * rh * rc;
+#else
       const double zeta = (be - al) / (2.0 * ga);
       const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
       const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+#endif
       for (int i = gl; i < p; i += G) {
         const double u = x[i], v = y[i];
         x[i] = c * u - s * v;

@@ -41,7 +41,8 @@ enum OpCode : int32_t {
   OP_D2LR = 9,      // M[m x n] -> (U', V', r)   (hmatrix.dense_to_lowrank)
   OP_SETRANK = 10,  // slot0 := dim0
   OP_APPEND = 11,   // hstack with zero padding (hmatrix.py:404-409,435-436)
-  OP_SVALS = 12     // sigma of G[p x q] (test entry point)
+  OP_SVALS = 12,    // sigma of G[p x q] (test entry point)
+  OP_TRSM_UN = 13   // B[n x c] := U^{-1} B        (back substitution, solve phase)
 };
 
 enum : int32_t { F_TA = 1, F_TB = 2, F_ACC = 4 };
@@ -497,7 +498,8 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       break;
     }
     case OP_TRSM_LL:
-    case OP_TRSM_UT: {
+    case OP_TRSM_UT:
+    case OP_TRSM_UN: {
       const int n = o.dim[0], cc = dimv(P, c, o.dim[1]);
       if (cc == 0 || n == 0) break;
       const double* T = mref(P, c, o.ref[0]);
@@ -508,11 +510,14 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       if (n <= 128 && n * n <= P.smem_work) {
         // multipliers staged as T[i + l n] (U transposed for the upper solve),
         // then one warp per group of columns, no block barriers
+        // (U reversed in both indices for the back substitution)
         if (o.code == OP_TRSM_LL) FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];
-        else FOR_MN(i, j, n, n) Ts[i + j * n] = T[j + (int64_t)i * ldt];
+        else if (o.code == OP_TRSM_UT) FOR_MN(i, j, n, n) Ts[i + j * n] = T[j + (int64_t)i * ldt];
+        else FOR_MN(i, j, n, n) Ts[i + j * n] = T[(n - 1 - i) + (int64_t)(n - 1 - j) * ldt];
         __syncthreads();
         if (o.code == OP_TRSM_LL) warp_trsm_cols<true>(n, cc, Ts, n, B, ldb);
-        else warp_trsm_cols<false>(n, cc, Ts, n, B, ldb);
+        else if (o.code == OP_TRSM_UT) warp_trsm_cols<false>(n, cc, Ts, n, B, ldb);
+        else warp_trsm_cols<false, true>(n, cc, Ts, n, B, ldb);
         __syncthreads();
         count(P, (double)n * n * cc, 8.0 * ((double)n * n / 2.0 + 2.0 * n * cc));
         break;
@@ -530,7 +535,8 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       double* Bw = stageB ? Bs : B;
       const int ldw = stageB ? n : ldb;
       if (o.code == OP_TRSM_LL) cta_trsm_lower_unit(n, cc, T, ldt, Bw, ldw);
-      else cta_trsm_upper_trans(n, cc, T, ldt, Bw, ldw);
+      else if (o.code == OP_TRSM_UT) cta_trsm_upper_trans(n, cc, T, ldt, Bw, ldw);
+      else cta_trsm_upper(n, cc, T, ldt, Bw, ldw);
       if (stageB) {
         FOR_MN(i, j, n, cc) B[i + (int64_t)j * ldb] = Bs[i + j * n];
         __syncthreads();
@@ -1442,6 +1448,12 @@ hmx_status hmx_trsm_upper_trans_batched(int32_t batch, int32_t n, int32_t c, con
                                         int32_t ldu, int64_t strideU, double* B, int32_t ldb,
                                         int64_t strideB, void* stream) {
   return trsm_batched(OP_TRSM_UT, batch, n, c, U, ldu, strideU, B, ldb, strideB, stream);
+}
+
+hmx_status hmx_trsm_upper_batched(int32_t batch, int32_t n, int32_t c, const double* U,
+                                  int32_t ldu, int64_t strideU, double* B, int32_t ldb,
+                                  int64_t strideB, void* stream) {
+  return trsm_batched(OP_TRSM_UN, batch, n, c, U, ldu, strideU, B, ldb, strideB, stream);
 }
 
 hmx_status hmx_gemm_batched(int32_t batch, int32_t m, int32_t n, int32_t k, double alpha,

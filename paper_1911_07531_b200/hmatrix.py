@@ -513,6 +513,28 @@ def hm_solve_upper_t(U: HMatrix, Y):
     return _dense_run(U, "solve_upper_t", Y, U.nrows)
 
 
+def hm_solve_upper(U: HMatrix, Y):
+    """Solve U X = Y, U upper triangular (non-unit), dense Y: block back
+    substitution, the non-transposed counterpart of hm_solve_upper_t
+    (hmatrix.py:331-341).  Solve phase with the factors (SURVEY.md 8(f)3);
+    the reference has no such entry point."""
+    if U.kind == LOWRANK:
+        raise ValueError("triangular solve on a low-rank diagonal block")
+    if U.nrows != U.ncols or U.nrows != Y.shape[0]:
+        raise ValueError("dimension mismatch in triangular solve")
+    return _dense_run(U, "solve_upper", Y, U.nrows)
+
+
+def lu_solve(L: HMatrix, U: HMatrix, B):
+    """X with L U X = B (A X ~ B after hlu / hlu_accu): forward substitution
+    with the unit-lower L, then back substitution with U, both on the
+    device over the H-matrix factors (cluster ordering: B and X are in the
+    permuted index order of the block tree, like A)."""
+    if L.table is not U.table or L.uid != U.uid:
+        raise ValueError("L and U are not over the same block")
+    return hm_solve_upper(U, hm_solve_lower(L, B))
+
+
 def lu_residual(A: HMatrix, L: HMatrix, U: HMatrix, X):
     """||A X - L (U X)||_F / ||A X||_F on the device (probe residual)."""
     AX = hm_apply(A, X)

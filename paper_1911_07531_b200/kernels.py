@@ -8,6 +8,7 @@ calls of the reference:
   getrf_nopiv        arith.dense_lu                      (arith.py:58-73)
   trsm_lower_unit    solve_triangular(lower, unit)       (hmatrix.py:321)
   trsm_upper_trans   solve_triangular(trans="T")         (hmatrix.py:334)
+  trsm_upper         solve_triangular(lower=False)       (solve phase, back substitution)
   gemm               the `@` products                    (hmatrix.py)
   truncate           hmatrix.truncate                    (hmatrix.py:113-130)
   dense_to_lowrank   hmatrix.dense_to_lowrank            (hmatrix.py:133-138)
@@ -86,6 +87,10 @@ def trsm_lower_unit(Ls, Bs):
 
 def trsm_upper_trans(Us, Bs):
     return _trsm(lib().hmx_trsm_upper_trans_batched, Us, Bs)
+
+
+def trsm_upper(Us, Bs):
+    return _trsm(lib().hmx_trsm_upper_batched, Us, Bs)
 
 
 def gemm(alpha, As, Bs, Cs=None, transA=False, transB=False, beta=0.0):

@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib as L
 from ._lib import (F_ACC, F_TA, F_TB, OP_ADD, OP_APPEND, OP_COPY, OP_D2LR, OP_GEMM, OP_LU,
-                   OP_SETRANK, OP_TRSM_LL, OP_TRSM_UT, OP_TRUNC, OP_ZERO, SCRATCH_BASE)
+                   OP_SETRANK, OP_TRSM_LL, OP_TRSM_UN, OP_TRSM_UT, OP_TRUNC, OP_ZERO, SCRATCH_BASE)
 from .trees import BlockTable
 
 ACC_BASE_ID = 3
@@ -423,6 +423,23 @@ class Planner:
         self.solve_upper_t(Um, k00, Y, cols, colsmax)
         self.hm_apply_t(Um, k01, Y, cols, colsmax, out=Y, alpha=-1.0, row_off=n0, fresh=False)
         self.solve_upper_t(Um, k11, Y.at(n0), cols, colsmax)
+
+    def solve_upper(self, Um: PMat, u, Y: Ref, cols, colsmax):
+        """Y := U[u]^{-1} Y, block back substitution (the non-transposed
+        counterpart of solve_upper_t; solve phase)."""
+        t = Um.t
+        if t.leaf[u]:
+            if t.adm[u]:
+                raise ValueError("triangular solve on a low-rank diagonal block")
+            self._op(OP_TRSM_UN, 0, (int(t.m[u]), cols, 0, 0), (int(t.m[u]), 0, Y.ld, 0),
+                     (Um.dense(u), None, Y, None))
+            return
+        k00, k01, _, k11 = (int(x) for x in t.kids[u])
+        n0 = int(t.m[k00])
+        self.solve_upper(Um, k11, Y.at(n0), cols, colsmax)
+        # Y[:n0] -= hm_apply(u01, Y[n0:])
+        self.hm_apply(Um, k01, Y.at(n0), cols, colsmax, out=Y, alpha=-1.0, row_off=0, fresh=False)
+        self.solve_upper(Um, k00, Y, cols, colsmax)
 
     # ------------------------------------------------------------------
     # product payloads (hmatrix.py:367-417)
@@ -1104,7 +1121,7 @@ def plan_op(table: BlockTable, op: str, policy, rank_cap=None, alpha=1.0, split_
     return prog
 
 
-DENSE_OPS = ("apply", "apply_t", "solve_lower", "solve_upper_t")
+DENSE_OPS = ("apply", "apply_t", "solve_lower", "solve_upper_t", "solve_upper")
 
 
 def _elementary(bounds_lo, bounds_hi, lo, hi):
@@ -1121,6 +1138,7 @@ def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
     apply_t:       out = H[u]^T @ X          X=1 (m_u x cols), out=2 (n_u x cols)
     solve_lower:   Y := L[u]^{-1} Y          L=0 unit lower, Y=1 (m_u x cols) in place
     solve_upper_t: Y := U[u]^{-T} Y          U=0 upper, Y=1 in place
+    solve_upper:   Y := U[u]^{-1} Y          U=0 upper, Y=1 in place (solve phase)
 
     apply / apply_t run one task per elementary row (column) interval of
     the leaves: each task owns its rows of the output and sums the
@@ -1191,6 +1209,8 @@ def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
         p.begin("dense_" + op, (op, u))
         if op == "solve_lower":
             p.solve_lower(H, u, Y, cols, cols)
+        elif op == "solve_upper":
+            p.solve_upper(H, u, Y, cols, cols)
         else:
             p.solve_upper_t(H, u, Y, cols, cols)
     prog = p.pack()

@@ -11,7 +11,7 @@ from paper_1911_07531_b200 import configs, hmatrix as H
 from paper_1911_07531_b200.planner import plan_dense
 
 
-@pytest.mark.parametrize("op", ["apply", "apply_t", "solve_lower", "solve_upper_t"])
+@pytest.mark.parametrize("op", ["apply", "apply_t", "solve_lower", "solve_upper_t", "solve_upper"])
 def test_dense_programs_build(op):
     cfg = configs.config("s2")
     _, _, _, broot = configs.structure(cfg)
@@ -70,6 +70,18 @@ def test_dense_ops_match_oracle(name):
         got = H.hm_solve_upper_t(H.HMatrix(U.store, uid), X[:m])
         want = O.solve_upper_t(Uh, uid, X[:m])
         assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+        got = H.hm_solve_upper(H.HMatrix(U.store, uid), X[:m])
+        want = O.solve_upper(Uh, uid, X[:m])
+        assert np.linalg.norm(got - want) <= 1e-10 * np.linalg.norm(want)
+    # solve phase: A x = b through the factors (forward + back substitution)
+    b = rng.normal(size=(n, 2))
+    x = H.lu_solve(L, U, b)
+    want = O.solve_upper(Uh, 0, O.solve_lower(Lh, 0, b))
+    assert np.linalg.norm(x - want) <= 1e-10 * np.linalg.norm(want)
+    # residual of the solve as good as the oracle's own solve with the same factors
+    r = np.linalg.norm(O.apply(Ah, 0, x) - b)
+    r_want = np.linalg.norm(O.apply(Ah, 0, want) - b)
+    assert r <= 2.0 * r_want + 1e-12 * np.linalg.norm(b)
     # vector right-hand side and the device probe residual
     y = H.hm_apply(A, X[:, 0])
     assert y.shape == (n,)

@@ -46,7 +46,7 @@ def test_trsm():
     from paper_1911_07531_b200 import kernels
 
     rng = np.random.default_rng(1)
-    for n, c in ((64, 64), (64, 7), (128, 20)):
+    for n, c in ((64, 64), (64, 7), (128, 20), (200, 5)):
         A = rng.normal(size=(n, n)) + n * np.eye(n)
         Lf = np.tril(A, -1) / n + np.eye(n)
         Uf = np.triu(A)
@@ -57,6 +57,10 @@ def test_trsm():
         W = kernels.trsm_upper_trans([Uf], [B])[0]
         Wr = sla.solve_triangular(Uf, B, trans="T", lower=False)
         assert np.linalg.norm(W - Wr) <= 1e-12 * np.linalg.norm(Wr)
+        # back substitution (solve phase): warp path n <= 128, CTA sweep above
+        Y = kernels.trsm_upper([Uf], [B])[0]
+        Yr = sla.solve_triangular(Uf, B, lower=False)
+        assert np.linalg.norm(Y - Yr) <= 1e-12 * np.linalg.norm(Yr)
 
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
