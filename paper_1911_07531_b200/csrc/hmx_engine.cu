@@ -189,7 +189,22 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
   const double thr = sig_out ? 0.0 : HMX_RRQR_THR * cut;  // see cta_rrqr
   unsigned long long t0 = P.trace ? gtimer2() : 0;
+#if HMX_WARPQR
+  int k;
+  if (q <= 64 && (ldg & 1)) {  // narrow core with a conflict-free layout: one warp
+    if (threadIdx.x < 32) {
+      k = warp_rrqr(p, q, G, ldg, tau, perm, thr);
+      if (threadIdx.x == 0) ired[0] = k;
+    }
+    __syncthreads();
+    k = ired[0];
+    __syncthreads();
+  } else {
+    k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
+  }
+#else
   const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
+#endif
   phase(P, 13, t0);
   double *X, *J;
   if (q * k + k * k > smcap && gevict && q * k + k * k <= smfullcap) {
@@ -322,7 +337,14 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* work = sm + 32;
   const int p = min(m, K), q = min(n, K);
   // stage U, V (and G) in shared memory when they fit
-  const int64_t need = (int64_t)(m + n) * K + 2 * K + (int64_t)p * q;
+#if HMX_WARPQR
+  // odd leading dimensions in shared memory (bank-conflict-free column-
+  // parallel access of the single-warp QR / RRQR)
+  const int ms = m | 1, ns = n | 1, pg = p | 1;
+#else
+  const int ms = m, ns = n, pg = p;
+#endif
+  const int64_t need = (int64_t)(ms + ns) * K + 2 * K + (int64_t)pg * q;
   const int Lmn = max(m, n);
   const int gre = pick_g(Lmn, min(min(m, n), K), HMX_THREADS);  // recomposition groups (r <= K)
   const int colneed = (HMX_THREADS / gre) * Lmn;
@@ -333,28 +355,38 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   int smcap;
   if (stage) {
     double* Us = work;
-    double* Vs = Us + m * K;
-    tau_u = Vs + n * K;
+    double* Vs = Us + ms * K;
+    tau_u = Vs + ns * K;
     tau_v = tau_u + K;
     G = tau_v + K;
-    FOR_MN(i, l, m, K) Us[i + l * m] = U[i + (int64_t)l * ldu];
-    FOR_MN(i, l, n, K) Vs[i + l * n] = V[i + (int64_t)l * ldv];
+    FOR_MN(i, l, m, K) Us[i + l * ms] = U[i + (int64_t)l * ldu];
+    FOR_MN(i, l, n, K) Vs[i + l * ns] = V[i + (int64_t)l * ldv];
     __syncthreads();
     U = Us;
     V = Vs;
-    // QR(U) on warps 0-3 and QR(V) on warps 4-7, concurrently
-    if ((threadIdx.x >> 5) < HMX_WARPS / 2)
-      group_householder_qr(m, K, U, m, tau_u, 0, HMX_WARPS / 2, 1);
-    else
-      group_householder_qr(n, K, V, n, tau_v, HMX_WARPS / 2, HMX_WARPS / 2, 2);
+#if HMX_WARPQR
+    if (K <= 64 && max(m, n) <= HMX_WARPQR_MAXM) {
+      // QR(U) on warp 0 and QR(V) on warp 1, one lane per column
+      const int w = threadIdx.x >> 5;
+      if (w == 0) warp_qr_cols(m, K, U, ms, tau_u);
+      else if (w == 1) warp_qr_cols(n, K, V, ns, tau_v);
+    } else
+#endif
+    {
+      // QR(U) on warps 0-3 and QR(V) on warps 4-7, concurrently
+      if ((threadIdx.x >> 5) < HMX_WARPS / 2)
+        group_householder_qr(m, K, U, ms, tau_u, 0, HMX_WARPS / 2, 1);
+      else
+        group_householder_qr(n, K, V, ns, tau_v, HMX_WARPS / 2, HMX_WARPS / 2, 2);
+    }
     __syncthreads();
     FOR_MN(i, j, p, q) {
       double acc = 0.0;
-      for (int l = max(i, j); l < K; ++l) acc = fma(U[i + l * m], V[j + l * n], acc);
-      G[i + j * p] = acc;
+      for (int l = max(i, j); l < K; ++l) acc = fma(U[i + l * ms], V[j + l * ns], acc);
+      G[i + j * pg] = acc;
     }
     __syncthreads();
-    smw = G + p * q;
+    smw = G + pg * q;
     smcap = (int)(P.smem_work - need);
   } else {
     cta_qr_blocked(m, K, U, ldu, tau_u, Vxu, m, Tu, Wq, work, P.smem_work, red);
@@ -371,12 +403,12 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     smw = gsm ? work + p * q : work;
     smcap = gsm ? P.smem_work - p * q : P.smem_work;
   }
-  const int ldu_q = stage ? m : ldu, ldv_q = stage ? n : ldv;
+  const int ldu_q = stage ? ms : ldu, ldv_q = stage ? ns : ldv;
   phase(P, 12, tq);
   double* Gq = nullptr;
   double* tau_g = nullptr;
   int ldgq = 0, kg = 0;
-  const int r = svd_lowrank(P, o, p, q, G, p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm, nullptr,
+  const int r = svd_lowrank(P, o, p, q, G, stage ? pg : p, ws2, smw, smcap, Uo, lduo, Vo, ldvo, sm, nullptr,
                             (!stage && G != Gg) ? Gg : nullptr, p, work, P.smem_work,
                             stage ? &Gq : nullptr, &ldgq, &tau_g, &kg);
   if (P.trace && threadIdx.x == 0) tq = gtimer2();
@@ -387,7 +419,7 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     // fused recomposition: U columns get Q_G then Q_u, V columns Q_v; one
     // lane group per column job, no block barriers between reflectors
     // column buffers after G (X/J are dead by now): colneed doubles
-    double* colbuf = colsm ? Gq + (int64_t)p * q : nullptr;
+    double* colbuf = colsm ? Gq + (int64_t)pg * q : nullptr;
     HMX_G_SWITCH(gre, (recompose_jobs<GG>(r, p, q, m, n, kg, Gq, ldgq, tau_g, U, ldu_q, tau_u,
                                                    V, ldv_q, tau_v, Uo, lduo, Vo, ldvo, colbuf)));
     __syncthreads();
@@ -418,15 +450,20 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* work = sm + 32;
   double* G = M;
   int ldg = ldm;
-  const bool gsm = m * n + 64 <= P.smem_work;
+#if HMX_WARPQR
+  const int ms = m | 1;  // odd: conflict-free column-parallel RRQR
+#else
+  const int ms = m;
+#endif
+  const bool gsm = ms * n + 64 <= P.smem_work;
   if (gsm) {
     G = work;
-    ldg = m;
-    FOR_MN(i, j, m, n) G[i + j * m] = M[i + (int64_t)j * ldm];
+    ldg = ms;
+    FOR_MN(i, j, m, n) G[i + j * ms] = M[i + (int64_t)j * ldm];
     __syncthreads();
   }
-  double* smw = gsm ? work + m * n : work;
-  const int smcap = gsm ? P.smem_work - m * n : P.smem_work;
+  double* smw = gsm ? work + ms * n : work;
+  const int smcap = gsm ? P.smem_work - ms * n : P.smem_work;
   const int r = svd_lowrank(P, o, m, n, G, ldg, ws, smw, smcap, Uo, o.ld[2], Vo, o.ld[3], sm,
                             nullptr, gsm ? M : nullptr, ldm, work, P.smem_work);
   if (threadIdx.x == 0) *rslot = r;
