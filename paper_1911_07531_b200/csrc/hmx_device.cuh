@@ -26,6 +26,12 @@
 #ifndef HMX_WARPQR_MAXM
 #define HMX_WARPQR_MAXM 512
 #endif
+#ifndef HMX_WARPJ
+#define HMX_WARPJ 0
+#endif
+#ifndef HMX_GSMALL
+#define HMX_GSMALL 0
+#endif
 #ifndef HMX_RRQR_THR
 #define HMX_RRQR_THR 1e-4
 #endif
@@ -282,6 +288,80 @@ __device__ __forceinline__ void gemm_splitk(int m, int n, int k, double alpha, c
   __syncthreads();
 }
 
+// Small-output GEMM (m*n <= 4*HMX_THREADS outputs, op(A) and op(B) fit the
+// shared work area): every load of op(A), op(B) and C is issued in one
+// pass (batches of 8 independent loads per thread), one barrier, then each
+// thread owns up to 4 outputs, each the same increasing-k fma chain as in
+// gemm_tiles (and the same epilogue), so the bits are identical.  Saves the
+// per-k-chunk barriers and exposed load latencies of the 64x64 tiling when
+// the output is a few rank x rank or m x rank blocks.
+__device__ __noinline__ void gemm_small(int m, int n, int k, double alpha, const double* __restrict__ A,
+                                        int lda, bool ta, const double* __restrict__ B, int ldb, bool tb,
+                                        bool beta1, double* C, int ldc, double* sm) {
+  const int kb = k | 1;
+  double* As = sm;          // op(A): As[i + kk*m]
+  double* Bs = sm + m * k;  // op(B): Bs[kk + j*kb]
+  const int tid = threadIdx.x;
+  const int mk = m * k, tot = mk + n * k;
+  const int mn = m * n;
+  double cv[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = tid + r * HMX_THREADS;
+    cv[r] = 0.0;
+    if (beta1 && e < mn) cv[r] = C[(e % m) + (int64_t)(e / m) * ldc];
+  }
+  for (int e0 = tid; e0 < tot; e0 += 8 * HMX_THREADS) {
+    double v[8];
+    int d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = e0 + q * HMX_THREADS;
+      d[q] = -1;
+      v[q] = 0.0;
+      if (e < mk) {
+        int i, kk;
+        if (!ta) { i = e % m; kk = e / m; v[q] = A[i + (int64_t)kk * lda]; }
+        else { kk = e % k; i = e / k; v[q] = A[kk + (int64_t)i * lda]; }
+        d[q] = i + kk * m;
+      } else if (e < tot) {
+        const int f = e - mk;
+        int j, kk;
+        if (!tb) { kk = f % k; j = f / k; v[q] = B[kk + (int64_t)j * ldb]; }
+        else { j = f % n; kk = f / n; v[q] = B[j + (int64_t)kk * ldb]; }
+        d[q] = mk + kk + j * kb;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (d[q] >= 0) sm[d[q]] = v[q];
+  }
+  __syncthreads();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int ii[4], jj[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = min(tid + r * HMX_THREADS, mn - 1);
+    ii[r] = e % m;
+    jj[r] = (e / m) * kb;
+  }
+  if (tid < mn) {
+    for (int kk = 0; kk < k; ++kk) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fma(As[ii[r] + kk * m], Bs[kk + jj[r]], acc[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = tid + r * HMX_THREADS;
+    if (e < mn) {
+      const double o = beta1 ? cv[r] + alpha * acc[r] : alpha * acc[r];
+      C[ii[r] + (int64_t)(jj[r] / kb) * ldc] = o;
+    }
+  }
+  __syncthreads();
+}
+
 // Inline GEMM of the op interpreter: the 64x64 tile shape only (every
 // extra instantiation raises the register pressure of the whole persistent
 // kernel).
@@ -369,8 +449,8 @@ __device__ void cta_trsm_lower_unit(int n, int c, const double* T, int ldt, doub
 
 __device__ void cta_trsm_upper_trans(int n, int c, const double* T, int ldt, double* B, int ldb) {
   for (int l = 0; l < n; ++l) {
-    const double d = T[l + (int64_t)l * ldt];
-    for (int j = threadIdx.x; j < c; j += HMX_THREADS) B[l + (int64_t)j * ldb] /= d;
+    const double rd = 1.0 / T[l + (int64_t)l * ldt];  // pivot reciprocal (OpenBLAS trsm convention)
+    for (int j = threadIdx.x; j < c; j += HMX_THREADS) B[l + (int64_t)j * ldb] *= rd;
     __syncthreads();
     const int r = n - l - 1;
     for (int e = threadIdx.x; e < r * c; e += HMX_THREADS) {
@@ -387,8 +467,8 @@ __device__ void cta_trsm_upper_trans(int n, int c, const double* T, int ldt, dou
 // pivots l = n-1 .. 0, divide row l, then eliminate it from rows 0..l-1.
 __device__ void cta_trsm_upper(int n, int c, const double* T, int ldt, double* B, int ldb) {
   for (int l = n - 1; l >= 0; --l) {
-    const double d = T[l + (int64_t)l * ldt];
-    for (int j = threadIdx.x; j < c; j += HMX_THREADS) B[l + (int64_t)j * ldb] /= d;
+    const double rd = 1.0 / T[l + (int64_t)l * ldt];
+    for (int j = threadIdx.x; j < c; j += HMX_THREADS) B[l + (int64_t)j * ldb] *= rd;
     __syncthreads();
     for (int e = threadIdx.x; e < l * c; e += HMX_THREADS) {
       const int i = e % l, j = e / l;
@@ -404,7 +484,8 @@ __device__ void cta_trsm_upper(int n, int c, const double* T, int ldt, double* B
 // upper solve).  Lane owns rows lane + 32q; a warp solves up to 4 columns of
 // B at once, keeping them in registers; the pivot value travels by shuffle.
 // Every element sees the same operations in the same order as the
-// CTA-wide sweeps above (bitwise-identical results).  REV addresses the
+// CTA-wide sweeps above (bitwise-identical results; for the non-unit
+// solves T's diagonal holds the pivot reciprocals 1/u_ll).  REV addresses the
 // rows of B in reverse (row n-1-i), which turns the back substitution of
 // an upper solve into this forward sweep (T staged reversed by the caller).
 template <bool UNIT, bool REV = false>
@@ -424,12 +505,14 @@ __device__ void warp_trsm_cols(int n, int c, const double* T, int ldt, double* B
       const int ql = l >> 5, ll = l & 31;
       double x[4];
       if (!UNIT) {
-        const double d = T[l + (int64_t)l * ldt];
+        // the caller stages the pivot reciprocals on the diagonal of T, so
+        // the pivot step is a multiply, not an fp64 divide, on the chain
+        const double rd = T[l + (int64_t)l * ldt];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (q == ql && lane == ll) {
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) b[cc][q] /= d;
+            for (int cc = 0; cc < 4; ++cc) b[cc][q] *= rd;
           }
       }
 #pragma unroll
@@ -703,6 +786,9 @@ __device__ void jacobi_rounds(int p, int q, double* Gm, int ldg, double* J, int 
   }
 }
 
+__device__ void jacobi_sigma_order(int p, int q, const double* G, int ldg, double* sigma,
+                                   int* order);
+
 __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int ldj,
                                double* sigma, int* order, int* flag, int* sweeps_out = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -729,7 +815,15 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
     __syncthreads();
   }
   if (sweeps_out) *sweeps_out = sweep;
-  // column norms
+  jacobi_sigma_order(p, q, G, ldg, sigma, order);
+  return converged;
+}
+
+// column norms sigma[q] of G and order[q] = columns by descending sigma
+// (ties by index); whole CTA, ends synchronised.
+__device__ void jacobi_sigma_order(int p, int q, const double* G, int ldg, double* sigma,
+                                   int* order) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int c = w; c < q; c += HMX_WARPS) {
     const double* g = G + (int64_t)c * ldg;
     double s = 0.0;
@@ -749,6 +843,79 @@ __device__ bool cta_jacobi_svd(int p, int q, double* G, int ldg, double* J, int 
     order[pos] = c;
   }
   __syncthreads();
+}
+
+// Single-warp one-sided Jacobi for q <= 64 columns (<= 32 pairs): lane =
+// pair of the round (same round-robin ordering, rotation and convergence
+// test as jacobi_rounds), dot products and rotations are serial loops of
+// the pair's lane, rounds are separated by __syncwarp only.  ldg and ldj
+// should be odd (conflict-free column-parallel access).
+__device__ __noinline__ bool warp_jacobi(int p, int q, double* Gm, int ldg, double* J, int ldj,
+                                         int* sweeps_out) {
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < q; c += 32)
+    for (int i = 0; i < q; ++i) J[i + (int64_t)c * ldj] = (i == c) ? 1.0 : 0.0;
+  __syncwarp();
+  const double tol2 = HMX_JACOBI_TOL * HMX_JACOBI_TOL;
+  const int qq = q + (q & 1);
+  const int npairs = qq / 2, mq = qq - 1;
+  bool converged = (q <= 1);
+  int sweep = 0;
+  for (; sweep < 60 && !converged; ++sweep) {
+    bool rot = false;
+    for (int rnd = 0; rnd < mq; ++rnd) {
+      const int pr = lane;
+      int a, b;
+      if (pr == 0) { a = 0; b = 1 + rnd; }
+      else {
+        a = pr + rnd; if (a >= mq) a -= mq;
+        a += 1;
+        b = mq - pr + rnd; if (b >= mq) b -= mq;
+        b += 1;
+      }
+      if (a > b) { const int t = a; a = b; b = t; }
+      if (pr < npairs && b < q) {
+        double* x = Gm + (int64_t)a * ldg;
+        double* y = Gm + (int64_t)b * ldg;
+        double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+        int i = 0;
+        for (; i + 1 < p; i += 2) {
+          const double u0 = x[i], v0 = y[i], u1 = x[i + 1], v1 = y[i + 1];
+          al0 = fma(u0, u0, al0); be0 = fma(v0, v0, be0); ga0 = fma(u0, v0, ga0);
+          al1 = fma(u1, u1, al1); be1 = fma(v1, v1, be1); ga1 = fma(u1, v1, ga1);
+        }
+        if (i < p) {
+          const double u0 = x[i], v0 = y[i];
+          al0 = fma(u0, u0, al0); be0 = fma(v0, v0, be0); ga0 = fma(u0, v0, ga0);
+        }
+        const double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+        if (al != 0.0 && be != 0.0 && ga * ga > tol2 * al * be) {
+          const double d = be - al, g2 = 2.0 * ga;
+          const double rh = rsqrt(fma(d, d, g2 * g2));
+          const double hc = fma(0.5 * fabs(d), rh, 0.5);
+          const double rc = rsqrt(hc);
+          const double c = hc * rc;
+          const double s = copysign(0.5, d) * g2 * rh * rc;
+          for (int r = 0; r < p; ++r) {
+            const double u = x[r], v = y[r];
+            x[r] = c * u - s * v;
+            y[r] = s * u + c * v;
+          }
+          double* ja = J + (int64_t)a * ldj;
+          double* jb = J + (int64_t)b * ldj;
+          for (int r = 0; r < q; ++r) {
+            const double u = ja[r], v = jb[r];
+            ja[r] = c * u - s * v;
+            jb[r] = s * u + c * v;
+          }
+          rot = true;
+        }
+      }
+      __syncwarp();
+    }
+    converged = !__any_sync(0xffffffffu, rot);
+  }
+  if (sweeps_out) *sweeps_out = sweep;
   return converged;
 }
 

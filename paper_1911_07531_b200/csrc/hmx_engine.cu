@@ -207,7 +207,17 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
 #endif
   phase(P, 13, t0);
   double *X, *J;
-  if (q * k + k * k > smcap && gevict && q * k + k * k <= smfullcap) {
+  int ldx = q, ldj = k;
+#if HMX_WARPJ
+  // single-warp Jacobi: odd leading dimensions when X and J sit in shared memory
+  const bool wj = k > 0 && k <= 64;
+  if (wj && (q | 1) * k + (k | 1) * k <= (gevict ? max(smcap, smfullcap) : smcap)) {
+    ldx = q | 1;
+    ldj = k | 1;
+  }
+#endif
+  const int xj = ldx * k + ldj * k;
+  if (xj > smcap && gevict && xj <= smfullcap) {
     // the Jacobi factors matter more than G: move G (R + reflectors) out of
     // shared memory and give the whole work area to X and J
     FOR_MN(i, c, p, q) gevict[i + (int64_t)c * ldevict] = G[i + (int64_t)c * ldg];
@@ -217,12 +227,24 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
     smw = smfull;
     smcap = smfullcap;
   }
-  if (q * k + k * k <= smcap) { X = smw; J = smw + q * k; }
-  else { X = rest; J = rest + (int64_t)q * k; }
-  FOR_MN(c, i, q, k) X[c + i * q] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
+  if (xj <= smcap) { X = smw; J = smw + ldx * k; }
+  else { ldx = q; ldj = k; X = rest; J = rest + (int64_t)q * k; }
+  FOR_MN(c, i, q, k) X[c + i * ldx] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
   __syncthreads();
   int sweeps = 0;
-  if (k > 0 && !cta_jacobi_svd(q, k, X, q, J, k, sig, ord, flag, &sweeps))
+#if HMX_WARPJ
+  if (wj) {
+    if (threadIdx.x < 32) {
+      const bool ok = warp_jacobi(q, k, X, ldx, J, ldj, &sweeps);
+      if (threadIdx.x == 0) { ired[2] = ok; ired[3] = sweeps; }
+    }
+    __syncthreads();
+    sweeps = ired[3];
+    if (!ired[2] && threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
+    jacobi_sigma_order(q, k, X, ldx, sig, ord);
+  } else
+#endif
+  if (k > 0 && !cta_jacobi_svd(q, k, X, ldx, J, ldj, sig, ord, flag, &sweeps))
     if (threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
   phase(P, 14, t0, sweeps);
   if (sig_out) {
@@ -239,11 +261,11 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   }
   FOR_MN(i, t, p, r) {
     const int col = ord[t];
-    dstU[i + (int64_t)t * ldu] = (i < k) ? J[i + col * k] * sig[col] : 0.0;
+    dstU[i + (int64_t)t * ldu] = (i < k) ? J[i + col * ldj] * sig[col] : 0.0;
   }
   FOR_MN(c, t, q, r) {
     const int col = ord[t];
-    dstV[perm[c] + (int64_t)t * ldv] = X[c + col * q] / sig[col];
+    dstV[perm[c] + (int64_t)t * ldv] = X[c + col * ldx] / sig[col];
   }
   __syncthreads();
   if (defer_g) {  // the caller fuses Q_G into its own recomposition
@@ -500,6 +522,12 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
         if (!acc) { cta_zero(m, n, C, o.ld[2]); __syncthreads(); }
         break;
       }
+#if HMX_GSMALL
+      if (m * n <= 4 * HMX_THREADS && k <= 1024 && m * k + (k | 1) * n <= P.smem_work)
+        gemm_small(m, n, k, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
+                   mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
+      else
+#endif
       cta_gemm(m, n, k, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
                mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
       count(P, 2.0 * m * n * k, 8.0 * ((double)m * k + (double)k * n + (double)m * n));
@@ -544,17 +572,27 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       double* B = mref(P, c, o.ref[2]);
       int ldb = o.ld[2];
       double* Ts = work;
-      if (n <= 128 && n * n <= P.smem_work) {
-        // multipliers staged as T[i + l n] (U transposed for the upper solve),
+      const int ns = n | 1;  // odd: the transposed staging writes are conflict-free
+      if (n <= 128 && ns * n <= P.smem_work) {
+        // multipliers staged as T[i + l ns] (U transposed for the upper solve),
         // then one warp per group of columns, no block barriers
-        // (U reversed in both indices for the back substitution)
-        if (o.code == OP_TRSM_LL) FOR_MN(i, j, n, n) Ts[i + j * n] = T[i + (int64_t)j * ldt];
-        else if (o.code == OP_TRSM_UT) FOR_MN(i, j, n, n) Ts[i + j * n] = T[j + (int64_t)i * ldt];
-        else FOR_MN(i, j, n, n) Ts[i + j * n] = T[(n - 1 - i) + (int64_t)(n - 1 - j) * ldt];
+        // (U reversed in both indices for the back substitution); the
+        // non-unit solves get the pivot reciprocals on the diagonal
+        if (o.code == OP_TRSM_LL) FOR_MN(i, j, n, n) Ts[i + j * ns] = T[i + (int64_t)j * ldt];
+        else if (o.code == OP_TRSM_UT)
+          FOR_MN(i, j, n, n) {  // coalesced read of U, transposed write
+            const double v = T[i + (int64_t)j * ldt];
+            Ts[j + i * ns] = (i == j) ? 1.0 / v : v;
+          }
+        else
+          FOR_MN(i, j, n, n) {
+            const double v = T[(n - 1 - i) + (int64_t)(n - 1 - j) * ldt];
+            Ts[i + j * ns] = (i == j) ? 1.0 / v : v;
+          }
         __syncthreads();
-        if (o.code == OP_TRSM_LL) warp_trsm_cols<true>(n, cc, Ts, n, B, ldb);
-        else if (o.code == OP_TRSM_UT) warp_trsm_cols<false>(n, cc, Ts, n, B, ldb);
-        else warp_trsm_cols<false, true>(n, cc, Ts, n, B, ldb);
+        if (o.code == OP_TRSM_LL) warp_trsm_cols<true>(n, cc, Ts, ns, B, ldb);
+        else if (o.code == OP_TRSM_UT) warp_trsm_cols<false>(n, cc, Ts, ns, B, ldb);
+        else warp_trsm_cols<false, true>(n, cc, Ts, ns, B, ldb);
         __syncthreads();
         count(P, (double)n * n * cc, 8.0 * ((double)n * n / 2.0 + 2.0 * n * cc));
         break;
