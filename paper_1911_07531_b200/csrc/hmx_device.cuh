@@ -20,15 +20,6 @@
 #ifndef HMX_JROT
 #define HMX_JROT 0
 #endif
-#ifndef HMX_WARPQR
-#define HMX_WARPQR 0
-#endif
-#ifndef HMX_WARPQR_MAXM
-#define HMX_WARPQR_MAXM 512
-#endif
-#ifndef HMX_WARPJ
-#define HMX_WARPJ 0
-#endif
 #ifndef HMX_GSMALL
 #define HMX_GSMALL 0
 #endif
@@ -845,80 +836,6 @@ __device__ void jacobi_sigma_order(int p, int q, const double* G, int ldg, doubl
   __syncthreads();
 }
 
-// Single-warp one-sided Jacobi for q <= 64 columns (<= 32 pairs): lane =
-// pair of the round (same round-robin ordering, rotation and convergence
-// test as jacobi_rounds), dot products and rotations are serial loops of
-// the pair's lane, rounds are separated by __syncwarp only.  ldg and ldj
-// should be odd (conflict-free column-parallel access).
-__device__ __noinline__ bool warp_jacobi(int p, int q, double* Gm, int ldg, double* J, int ldj,
-                                         int* sweeps_out) {
-  const int lane = threadIdx.x & 31;
-  for (int c = lane; c < q; c += 32)
-    for (int i = 0; i < q; ++i) J[i + (int64_t)c * ldj] = (i == c) ? 1.0 : 0.0;
-  __syncwarp();
-  const double tol2 = HMX_JACOBI_TOL * HMX_JACOBI_TOL;
-  const int qq = q + (q & 1);
-  const int npairs = qq / 2, mq = qq - 1;
-  bool converged = (q <= 1);
-  int sweep = 0;
-  for (; sweep < 60 && !converged; ++sweep) {
-    bool rot = false;
-    for (int rnd = 0; rnd < mq; ++rnd) {
-      const int pr = lane;
-      int a, b;
-      if (pr == 0) { a = 0; b = 1 + rnd; }
-      else {
-        a = pr + rnd; if (a >= mq) a -= mq;
-        a += 1;
-        b = mq - pr + rnd; if (b >= mq) b -= mq;
-        b += 1;
-      }
-      if (a > b) { const int t = a; a = b; b = t; }
-      if (pr < npairs && b < q) {
-        double* x = Gm + (int64_t)a * ldg;
-        double* y = Gm + (int64_t)b * ldg;
-        double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
-        int i = 0;
-        for (; i + 1 < p; i += 2) {
-          const double u0 = x[i], v0 = y[i], u1 = x[i + 1], v1 = y[i + 1];
-          al0 = fma(u0, u0, al0); be0 = fma(v0, v0, be0); ga0 = fma(u0, v0, ga0);
-          al1 = fma(u1, u1, al1); be1 = fma(v1, v1, be1); ga1 = fma(u1, v1, ga1);
-        }
-        if (i < p) {
-          const double u0 = x[i], v0 = y[i];
-          al0 = fma(u0, u0, al0); be0 = fma(v0, v0, be0); ga0 = fma(u0, v0, ga0);
-        }
-        const double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
-        if (al != 0.0 && be != 0.0 && ga * ga > tol2 * al * be) {
-          const double d = be - al, g2 = 2.0 * ga;
-          const double rh = rsqrt(fma(d, d, g2 * g2));
-          const double hc = fma(0.5 * fabs(d), rh, 0.5);
-          const double rc = rsqrt(hc);
-          const double c = hc * rc;
-          const double s = copysign(0.5, d) * g2 * rh * rc;
-          for (int r = 0; r < p; ++r) {
-            const double u = x[r], v = y[r];
-            x[r] = c * u - s * v;
-            y[r] = s * u + c * v;
-          }
-          double* ja = J + (int64_t)a * ldj;
-          double* jb = J + (int64_t)b * ldj;
-          for (int r = 0; r < q; ++r) {
-            const double u = ja[r], v = jb[r];
-            ja[r] = c * u - s * v;
-            jb[r] = s * u + c * v;
-          }
-          rot = true;
-        }
-      }
-      __syncwarp();
-    }
-    converged = !__any_sync(0xffffffffu, rot);
-  }
-  if (sweeps_out) *sweeps_out = sweep;
-  return converged;
-}
-
 // ---------------------------------------------------------------------------
 // Rank-revealing QR: column-pivoted Householder QR (LAPACK dgeqp3 / dlaqp2
 // conventions) of the p x q matrix G, stopped after k steps as soon as the
@@ -1047,192 +964,6 @@ __device__ int cta_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm
     __syncthreads();
   }
   return kmax;
-}
-
-// ---------------------------------------------------------------------------
-// Single-warp, lane-per-column variants for narrow factors (K <= 64) staged
-// in shared memory: lane l owns columns l and l + 32; the Householder
-// vector of step j is read by all lanes as a broadcast, every column's dot
-// product and update is a serial loop of its owner lane, and a step needs
-// only __syncwarp -- no block barrier and no shuffle reduction per column.
-// The shared-memory leading dimension should be odd so that the 32 lanes
-// reading row i of 32 columns hit distinct banks.  The reflector
-// convention (dlarfg, v_j = 1, R in the upper triangle) and the RRQR
-// pivoting/stopping rules are those of qr_steps / cta_rrqr above; only the
-// summation order of the dot products differs.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double col_sumsq(const double* x, int i0, int m) {
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int i = i0;
-  for (; i + 3 < m; i += 4) {
-    s0 = fma(x[i], x[i], s0);
-    s1 = fma(x[i + 1], x[i + 1], s1);
-    s2 = fma(x[i + 2], x[i + 2], s2);
-    s3 = fma(x[i + 3], x[i + 3], s3);
-  }
-  for (; i < m; ++i) s0 = fma(x[i], x[i], s0);
-  return (s0 + s1) + (s2 + s3);
-}
-
-// y := (I - t v v^T) y over rows j..m-1, v_j = 1 implicit (v = x).
-__device__ __forceinline__ void col_apply(const double* x, double t, double* y, int j, int m) {
-  double d0 = y[j], d1 = 0.0, d2 = 0.0, d3 = 0.0;
-  int i = j + 1;
-  for (; i + 2 < m; i += 3) {
-    d1 = fma(x[i], y[i], d1);
-    d2 = fma(x[i + 1], y[i + 1], d2);
-    d3 = fma(x[i + 2], y[i + 2], d3);
-  }
-  for (; i < m; ++i) d1 = fma(x[i], y[i], d1);
-  const double d = ((d0 + d1) + (d2 + d3)) * t;
-  y[j] -= d;
-  for (i = j + 1; i < m; ++i) y[i] = fma(-d, x[i], y[i]);
-}
-
-// Builds the reflector of column x (rows j..m-1) in place; returns tau.
-__device__ __forceinline__ double col_reflector(double* x, int j, int m) {
-  const double ss = col_sumsq(x, j + 1, m);
-  const double alpha = x[j];
-  if (!(ss > 0.0)) return 0.0;
-  const double beta = -copysign(sqrt(alpha * alpha + ss), alpha);
-  const double t = (beta - alpha) / beta;
-  const double scal = 1.0 / (alpha - beta);
-  for (int i = j + 1; i < m; ++i) x[i] *= scal;
-  x[j] = beta;
-  return t;
-}
-
-// Householder QR of m x K (K <= 64) by the calling warp.
-__device__ __noinline__ void warp_qr_cols(int m, int K, double* A, int lda, double* tau) {
-  const int lane = threadIdx.x & 31;
-  const int p = min(m, K);
-  for (int j = 0; j < p; ++j) {
-    double* x = A + (int64_t)j * lda;
-    double t = 0.0;
-    if (lane == (j & 31)) {
-      t = col_reflector(x, j, m);
-      tau[j] = t;
-    }
-    __syncwarp();
-    t = __shfl_sync(0xffffffffu, t, j & 31);
-    if (t != 0.0) {
-      for (int c = lane; c < K; c += 32)
-        if (c > j) col_apply(x, t, A + (int64_t)c * lda, j, m);
-    }
-    __syncwarp();
-  }
-}
-
-// Column-pivoted QR of p x q (q <= 64) by the calling warp, the semantics
-// of cta_rrqr (same pivot rule, ties to the lower index, same stopping
-// test on the trailing Frobenius norm, dlaqp2 norm downdates).
-__device__ __noinline__ int warp_rrqr(int p, int q, double* G, int ldg, double* tau, int* perm,
-                                      double thr) {
-  const int lane = threadIdx.x & 31;
-  double cn[2], cn0[2];
-  int pm[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int c = lane + 32 * s;
-    cn[s] = (c < q) ? col_sumsq(G + (int64_t)c * ldg, 0, p) : 0.0;
-    cn0[s] = cn[s];
-    pm[s] = c;
-  }
-  const int kmax = min(p, q);
-  double r00sq = 0.0;
-  int k = kmax;
-  for (int j = 0; j < kmax; ++j) {
-    double v, tail;
-    int idx;
-    bool stop = false;
-    for (int pass = 0; pass < 2; ++pass) {
-      v = -1.0; tail = 0.0; idx = -1;
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int c = lane + 32 * s;
-        if (c >= j && c < q) {
-          tail += cn[s];
-          if (cn[s] > v) { v = cn[s]; idx = c; }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-        tail += __shfl_xor_sync(0xffffffffu, tail, o);
-        if (ov > v || (ov == v && oi >= 0 && (idx < 0 || oi < idx))) { v = ov; idx = oi; }
-      }
-      if (j == 0 && pass == 0) r00sq = v;
-      if (!(v > 0.0)) { stop = true; break; }
-      const double lim = thr * thr * r00sq;
-      if (pass == 1) {
-        stop = tail <= lim;
-        break;
-      }
-      if (!(tail <= 4.0 * lim)) break;
-      // exact trailing norms near the cut, then decide again
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int c = lane + 32 * s;
-        if (c >= j && c < q) {
-          cn[s] = col_sumsq(G + (int64_t)c * ldg, j, p);
-          cn0[s] = cn[s];
-        }
-      }
-    }
-    if (stop) { k = j; break; }
-    if (idx != j) {
-      // swap positional columns j and idx: rows by the whole warp, the
-      // owners exchange norms and permutation entries
-      double* a = G + (int64_t)j * ldg;
-      double* b = G + (int64_t)idx * ldg;
-      for (int i = lane; i < p; i += 32) {
-        const double tt = a[i];
-        a[i] = b[i];
-        b[i] = tt;
-      }
-      const int sj = j >> 5, si = idx >> 5;
-      const double cj = __shfl_sync(0xffffffffu, sj ? cn[1] : cn[0], j & 31);
-      const double c0j = __shfl_sync(0xffffffffu, sj ? cn0[1] : cn0[0], j & 31);
-      const int pj = __shfl_sync(0xffffffffu, sj ? pm[1] : pm[0], j & 31);
-      const double ci = __shfl_sync(0xffffffffu, si ? cn[1] : cn[0], idx & 31);
-      const double c0i = __shfl_sync(0xffffffffu, si ? cn0[1] : cn0[0], idx & 31);
-      const int pi = __shfl_sync(0xffffffffu, si ? pm[1] : pm[0], idx & 31);
-      if (lane == (j & 31)) { cn[sj] = ci; cn0[sj] = c0i; pm[sj] = pi; }
-      if (lane == (idx & 31)) { cn[si] = cj; cn0[si] = c0j; pm[si] = pj; }
-      __syncwarp();
-    }
-    double* x = G + (int64_t)j * ldg;
-    double t = 0.0;
-    if (lane == (j & 31)) {
-      t = col_reflector(x, j, p);
-      tau[j] = t;
-    }
-    __syncwarp();
-    t = __shfl_sync(0xffffffffu, t, j & 31);
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int c = lane + 32 * s;
-      if (c > j && c < q) {
-        double* y = G + (int64_t)c * ldg;
-        if (t != 0.0) col_apply(x, t, y, j, p);
-        const double rj = y[j];
-        const double nv = cn[s] - rj * rj;
-        if (!(nv > 1e-4 * cn0[s])) {
-          cn[s] = col_sumsq(y, j + 1, p);
-          cn0[s] = cn[s];
-        } else {
-          cn[s] = nv;
-        }
-      }
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int s = 0; s < 2; ++s)
-    if (lane + 32 * s < q) perm[lane + 32 * s] = pm[s];
-  __syncwarp();
-  return k;
 }
 
 // ---------------------------------------------------------------------------

@@ -189,33 +189,10 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
   const double thr = sig_out ? 0.0 : HMX_RRQR_THR * cut;  // see cta_rrqr
   unsigned long long t0 = P.trace ? gtimer2() : 0;
-#if HMX_WARPQR
-  int k;
-  if (q <= 64 && (ldg & 1)) {  // narrow core with a conflict-free layout: one warp
-    if (threadIdx.x < 32) {
-      k = warp_rrqr(p, q, G, ldg, tau, perm, thr);
-      if (threadIdx.x == 0) ired[0] = k;
-    }
-    __syncthreads();
-    k = ired[0];
-    __syncthreads();
-  } else {
-    k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
-  }
-#else
   const int k = cta_rrqr(p, q, G, ldg, tau, perm, cn, cn0, thr, red, ired);
-#endif
   phase(P, 13, t0);
   double *X, *J;
   int ldx = q, ldj = k;
-#if HMX_WARPJ
-  // single-warp Jacobi: odd leading dimensions when X and J sit in shared memory
-  const bool wj = k > 0 && k <= 64;
-  if (wj && (q | 1) * k + (k | 1) * k <= (gevict ? max(smcap, smfullcap) : smcap)) {
-    ldx = q | 1;
-    ldj = k | 1;
-  }
-#endif
   const int xj = ldx * k + ldj * k;
   if (xj > smcap && gevict && xj <= smfullcap) {
     // the Jacobi factors matter more than G: move G (R + reflectors) out of
@@ -232,18 +209,6 @@ __device__ int svd_lowrank(const DevPlan& P, const hmx_op& o, int p, int q, doub
   FOR_MN(c, i, q, k) X[c + i * ldx] = (c >= i) ? G[i + (int64_t)c * ldg] : 0.0;
   __syncthreads();
   int sweeps = 0;
-#if HMX_WARPJ
-  if (wj) {
-    if (threadIdx.x < 32) {
-      const bool ok = warp_jacobi(q, k, X, ldx, J, ldj, &sweeps);
-      if (threadIdx.x == 0) { ired[2] = ok; ired[3] = sweeps; }
-    }
-    __syncthreads();
-    sweeps = ired[3];
-    if (!ired[2] && threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
-    jacobi_sigma_order(q, k, X, ldx, sig, ord);
-  } else
-#endif
   if (k > 0 && !cta_jacobi_svd(q, k, X, ldx, J, ldj, sig, ord, flag, &sweeps))
     if (threadIdx.x == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
   phase(P, 14, t0, sweeps);
@@ -359,13 +324,7 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* work = sm + 32;
   const int p = min(m, K), q = min(n, K);
   // stage U, V (and G) in shared memory when they fit
-#if HMX_WARPQR
-  // odd leading dimensions in shared memory (bank-conflict-free column-
-  // parallel access of the single-warp QR / RRQR)
-  const int ms = m | 1, ns = n | 1, pg = p | 1;
-#else
   const int ms = m, ns = n, pg = p;
-#endif
   const int64_t need = (int64_t)(ms + ns) * K + 2 * K + (int64_t)pg * q;
   const int Lmn = max(m, n);
   const int gre = pick_g(Lmn, min(min(m, n), K), HMX_THREADS);  // recomposition groups (r <= K)
@@ -386,14 +345,6 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
     __syncthreads();
     U = Us;
     V = Vs;
-#if HMX_WARPQR
-    if (K <= 64 && max(m, n) <= HMX_WARPQR_MAXM) {
-      // QR(U) on warp 0 and QR(V) on warp 1, one lane per column
-      const int w = threadIdx.x >> 5;
-      if (w == 0) warp_qr_cols(m, K, U, ms, tau_u);
-      else if (w == 1) warp_qr_cols(n, K, V, ns, tau_v);
-    } else
-#endif
     {
       // QR(U) on warps 0-3 and QR(V) on warps 4-7, concurrently
       if ((threadIdx.x >> 5) < HMX_WARPS / 2)
@@ -472,11 +423,7 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* work = sm + 32;
   double* G = M;
   int ldg = ldm;
-#if HMX_WARPQR
-  const int ms = m | 1;  // odd: conflict-free column-parallel RRQR
-#else
   const int ms = m;
-#endif
   const bool gsm = ms * n + 64 <= P.smem_work;
   if (gsm) {
     G = work;
