@@ -4,8 +4,8 @@
  * Replaces the refinement DAG construction of the reference
  * (hmatdag/taskgraph.py:530-665, compute_dag / build_hlu_dag, Alg. 10-12 and
  * 14-15 of arXiv 1911.07531) with the same node and edge sets (tests compare
- * them with the reference's own DAGs).  Sparsification (taskgraph.py:384-432)
- * is not offered here.
+ * them with the reference's own DAGs), optionally with the reference's edge
+ * sparsification (Alg. 13, taskgraph.py:360-432).
  */
 #ifndef HMX_DAG_H
 #define HMX_DAG_H
@@ -30,6 +30,15 @@ int hmx_dag_build(int32_t n_blocks, const int64_t* r0, const int64_t* r1, const 
                   const int64_t* c1, const int8_t* leaf, const int32_t* parent,
                   const int32_t* kids, int32_t mode, int64_t stop_size, int32_t root_op,
                   hmx_dag** out);
+/* hmx_dag_build plus edge sparsification per refinement round
+ * (build_hlu_dag / compute_dag with sparsify=True, max_path_len,
+ * taskgraph.py:530-590, 636-665): the same node set, the reference's
+ * sparsified edge set.  Returns 1 for sparsify in mode 1 (the reference's
+ * ValueError, taskgraph.py:652-653) or max_path_len < 1. */
+int hmx_dag_build_ex(int32_t n_blocks, const int64_t* r0, const int64_t* r1, const int64_t* c0,
+                     const int64_t* c1, const int8_t* leaf, const int32_t* parent,
+                     const int32_t* kids, int32_t mode, int64_t stop_size, int32_t root_op,
+                     int32_t sparsify, int32_t max_path_len, hmx_dag** out);
 int64_t hmx_dag_nodes(const hmx_dag* dag);
 int64_t hmx_dag_edges(const hmx_dag* dag);
 /* Nodes in creation-sequence order (TaskGraph.nodes): kind code (0 hlu,

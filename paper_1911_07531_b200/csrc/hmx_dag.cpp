@@ -9,7 +9,9 @@
 // (mutual matches directed by creation order), inherited edges are narrowed
 // to sub-tasks, and unrefined tasks retire once their successor sets stop
 // changing.  The merged accumulator mode stitches the shift/apply tree of
-// the block tree to the arithmetic graph.  Sparsification stays in Python.
+// the block tree to the arithmetic graph.  Edge sparsification (Alg. 13,
+// taskgraph.py:360-432) runs per refinement round against one snapshot of
+// the round's edge state, as in the reference.
 //
 // Tasks live in one arena (indices are stable); successor sets are sorted
 // unique int vectors.  Results are independent of container iteration
@@ -19,6 +21,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <iterator>
 #include <new>
 #include <vector>
 
@@ -257,6 +260,75 @@ struct hmx_dag {  // the opaque handle of include/hmx_dag.h
   std::vector<int32_t> idx;
 };
 
+namespace {
+
+// Alg. 13 over one refinement round (taskgraph.py:384-432, _sparsify_batch):
+// for every target t, the neighbourhood n = (sub-tasks of t, or t) plus the
+// successors of t (their sub-tasks when refined); every pruned task tp
+// (t's sub-tasks, or t) loses the successors that are also reachable from
+// it by a path of length in [2, cap] inside n (remove_redundant /
+// _bfs_ge2, taskgraph.py:360-381).  All decisions read the round's edge
+// state before any removal is committed, so the result is independent of
+// the target order.
+struct Sparsifier {
+  std::vector<int32_t> in_n, seen, out;  // epoch stamps per task id
+  int32_t ep_n = 0, ep = 0;
+
+  void fit(size_t n) {
+    if (in_n.size() < n) { in_n.resize(n, 0); seen.resize(n, 0); out.resize(n, 0); }
+  }
+
+  void run(std::vector<Task>& T, const std::vector<int32_t>& targets, int cap) {
+    fit(T.size());
+    std::vector<std::pair<int32_t, std::vector<int32_t>>> dec;
+    std::vector<int32_t> frontier, nxt;
+    for (int32_t t : targets) {
+      const Task& tt = T[t];
+      ++ep_n;
+      auto mark = [&](int32_t u) { in_n[u] = ep_n; };
+      if (tt.nsub) for (int32_t x = 0; x < tt.nsub; ++x) mark((int32_t)(tt.sub0 + x));
+      else mark(t);
+      for (int32_t h : tt.succ) {
+        const Task& th = T[h];
+        if (th.nsub) for (int32_t y = 0; y < th.nsub; ++y) mark((int32_t)(th.sub0 + y));
+        else mark(h);
+      }
+      const int32_t np = tt.nsub ? tt.nsub : 1;
+      for (int32_t x = 0; x < np; ++x) {
+        const int32_t tp = tt.nsub ? (int32_t)(tt.sub0 + x) : t;
+        ++ep;
+        frontier.clear();
+        for (int32_t s : T[tp].succ)
+          if (in_n[s] == ep_n) { frontier.push_back(s); seen[s] = ep; }
+        for (int depth = 1; !frontier.empty() && depth < cap; ++depth) {
+          nxt.clear();
+          for (int32_t u : frontier)
+            for (int32_t v : T[u].succ)
+              if (in_n[v] == ep_n) {
+                out[v] = ep;
+                if (seen[v] != ep) { seen[v] = ep; nxt.push_back(v); }
+              }
+          frontier.swap(nxt);
+        }
+        std::vector<int32_t> rem;
+        for (int32_t s : T[tp].succ)
+          if (out[s] == ep) rem.push_back(s);
+        if (!rem.empty()) dec.emplace_back(tp, std::move(rem));
+      }
+    }
+    for (auto& d : dec) {  // commit (successor sets and rem are sorted)
+      std::vector<int32_t>& s = T[d.first].succ;
+      std::vector<int32_t> keep;
+      keep.reserve(s.size());
+      std::set_difference(s.begin(), s.end(), d.second.begin(), d.second.end(),
+                          std::back_inserter(keep));
+      s.swap(keep);
+    }
+  }
+};
+
+}  // namespace
+
 extern "C" {
 
 // Builds the H-LU (root_op 0) or standalone multiply / solve (1 hmul,
@@ -266,7 +338,21 @@ extern "C" {
 int hmx_dag_build(int32_t nb, const int64_t* r0, const int64_t* r1, const int64_t* c0,
                   const int64_t* c1, const int8_t* leaf, const int32_t* parent, const int32_t* kids,
                   int32_t mode, int64_t stop_size, int32_t root_op, hmx_dag** out) {
+  return hmx_dag_build_ex(nb, r0, r1, c0, c1, leaf, parent, kids, mode, stop_size, root_op, 0, 2,
+                          out);
+}
+
+// As hmx_dag_build, plus edge sparsification (compute_dag's sparsify /
+// max_path_len, taskgraph.py:530-590); not valid in combined mode
+// (taskgraph.py:652-653).
+int hmx_dag_build_ex(int32_t nb, const int64_t* r0, const int64_t* r1, const int64_t* c0,
+                     const int64_t* c1, const int8_t* leaf, const int32_t* parent,
+                     const int32_t* kids, int32_t mode, int64_t stop_size, int32_t root_op,
+                     int32_t sparsify, int32_t max_path_len, hmx_dag** out) {
   if (!out || nb <= 0 || mode < 0 || mode > 2) return 1;
+  if (sparsify && (mode == M_COMBINED || max_path_len < 1)) return 1;
+  Sparsifier sp;
+  std::vector<int32_t> starg;
   Builder b{nb, r0, r1, c0, c1, leaf, parent, kids, mode, stop_size, {}};
   b.T.reserve(1 << 16);
   const std::vector<int32_t> rseq{mode == M_MERGED ? 1 : 0};
@@ -288,9 +374,11 @@ int hmx_dag_build(int32_t nb, const int64_t* r0, const int64_t* r1, const int64_
       if (b.T[g].nsub == 0 && b.refinable(b.T[g]))
         if (!b.refine(g)) return 2;
     nxt.clear();
+    starg.clear();
     for (int32_t g : current) {
       Task& tg = b.T[g];
       if (tg.nsub) {
+        if (sparsify) starg.push_back(g);
         // inherited edges become edges between sub-tasks
         const std::vector<int32_t> succ = tg.succ;
         for (int32_t h : succ) {
@@ -327,9 +415,11 @@ int hmx_dag_build(int32_t nb, const int64_t* r0, const int64_t* r1, const int64_
           nxt.push_back(g);
         } else {
           retired.push_back(g);
+          if (sparsify) starg.push_back(g);
         }
       }
     }
+    if (sparsify && !starg.empty()) sp.run(b.T, starg, max_path_len);
     current.swap(nxt);
   }
   std::vector<int32_t> nodes = retired;

@@ -230,10 +230,9 @@ class ExecPlan:
             prog = fuse_applies(prog)
             self.prog = prog
         self.dag_mode = dag_mode
-        # the reference DAG: native builder (bit-exact, ~25x faster) unless
-        # sparsified (Python builder)
-        self.dag = (tg.build_hlu_dag(table, dag_mode, sparsify=True) if sparsify
-                    else tg.build_dag_native(table, dag_mode))
+        # the reference DAG (sparsified or not): native builder (bit-exact,
+        # ~25x faster than the Python one)
+        self.dag = tg.build_dag_native(table, dag_mode, sparsify=sparsify)
         ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()
         self.succ_ptr, self.succ_idx = ptr, idx
         lv = tg.asap_levels(len(prog.keys), ptr, idx)

@@ -701,6 +701,9 @@ def _native():
         vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
         L.hmx_dag_build.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, i64, i32, C.POINTER(vp)]
         L.hmx_dag_build.restype = C.c_int
+        L.hmx_dag_build_ex.argtypes = [i32, vp, vp, vp, vp, vp, vp, vp, i32, i64, i32, i32, i32,
+                                       C.POINTER(vp)]
+        L.hmx_dag_build_ex.restype = C.c_int
         L.hmx_dag_nodes.argtypes = [vp]
         L.hmx_dag_nodes.restype = i64
         L.hmx_dag_edges.argtypes = [vp]
@@ -768,13 +771,19 @@ class NativeTaskGraph:
         return asap_levels(len(self.nodes), *self.csr(), extra_edges)
 
 
-def build_dag_native(block_root, mode: str = STD, *, stop_size: int = 0, op: str = "hlu"):
+def build_dag_native(block_root, mode: str = STD, *, stop_size: int = 0, op: str = "hlu",
+                     sparsify: bool = False, max_path_len: int = 2):
     """Native (C++) refinement build; same node and edge sets as
-    build_hlu_dag / compute_dag without sparsification."""
+    build_hlu_dag / compute_dag, with or without edge sparsification
+    (taskgraph.py:384-432, applied per refinement round)."""
     import ctypes as C
 
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
+    if mode == COMBINED and sparsify:
+        raise ValueError("edge sparsification is not valid in combined accumulator mode")
+    if max_path_len < 1:
+        raise ValueError("max_path_len must be >= 1")
     t = _as_table(block_root)
     L = _native()
     arr = [np.ascontiguousarray(x, dtype=np.int64) for x in (t.r0, t.r1, t.c0, t.c1)]
@@ -782,8 +791,9 @@ def build_dag_native(block_root, mode: str = STD, *, stop_size: int = 0, op: str
     parent = np.ascontiguousarray(t.parent, dtype=np.int32)
     kids = np.ascontiguousarray(np.where(t.kids < 0, -1, t.kids), dtype=np.int32).reshape(-1, 4)
     h = C.c_void_p()
-    rc = L.hmx_dag_build(t.n, *[a.ctypes.data for a in arr], leaf.ctypes.data, parent.ctypes.data,
-                         kids.ctypes.data, _MODE_CODE[mode], int(stop_size), _OP_CODE[op], C.byref(h))
+    rc = L.hmx_dag_build_ex(t.n, *[a.ctypes.data for a in arr], leaf.ctypes.data, parent.ctypes.data,
+                            kids.ctypes.data, _MODE_CODE[mode], int(stop_size), _OP_CODE[op],
+                            int(bool(sparsify)), int(max_path_len), C.byref(h))
     if rc == 2:
         raise ValueError("structural error in refinement (leaf diagonal / operands)")
     if rc == 3:

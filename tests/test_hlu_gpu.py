@@ -34,7 +34,8 @@ def product_structure(name):
     return cfg, broot, perm
 
 
-def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256, dag_mode=None):
+def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256, dag_mode=None,
+               sparsify=False):
     from paper_1911_07531_b200 import hmatrix as H
     from paper_1911_07531_b200.accumulator import AccumulatorMap, hlu_accu
     from paper_1911_07531_b200.arith import hlu
@@ -45,10 +46,10 @@ def run_device(name, mode, A_leaves, exec_mode=2, rank_cap=64, split_min=256, da
     L, U = H.zeros(broot, pol, rank_cap), H.zeros(broot, pol, rank_cap)
     H.counters.reset()
     if mode == "std":
-        plan = hlu(A, L, U, pol, exec_mode=exec_mode, split_min=split_min)
+        plan = hlu(A, L, U, pol, exec_mode=exec_mode, split_min=split_min, sparsify=sparsify)
     else:
         plan = hlu_accu(A, L, U, AccumulatorMap(), pol, exec_mode=exec_mode, split_min=split_min,
-                        dag_mode=dag_mode)
+                        dag_mode=dag_mode, sparsify=sparsify)
     return L.store.download_leaves(), U.store.download_leaves(), H.counters.snapshot(), plan
 
 
@@ -85,6 +86,22 @@ def test_combined_mode_equals_merged():
     a = run_device("s2", "accu", A.lv, dag_mode="accu-merged")
     b = run_device("s2", "accu", A.lv, dag_mode="accu-combined")
     assert b[3].n_tasks == 5241 + 80 or b[3].dag.n_nodes == 5241
+    for x, y in zip(a[:2], b[:2]):
+        for u, v in x.items():
+            for p, q in zip(v[1:], y[u][1:]):
+                assert np.array_equal(p, q)
+    assert a[2] == b[2]
+
+
+@pytest.mark.parametrize("mode", ["std", "accu"])
+def test_sparsified_dag_execution_bitwise_identical(mode):
+    """Executing the sparsified DAG (native Alg. 13, same transitive
+    closure) gives the bits of the full DAG, with fewer device edges."""
+    A, pol, eps = oracle_A("s2")
+    a = run_device("s2", mode, A.lv, split_min=32)
+    b = run_device("s2", mode, A.lv, split_min=32, sparsify=True)
+    assert b[3].dag.n_edges < a[3].dag.n_edges
+    assert b[3].n_dag_edges <= a[3].n_dag_edges
     for x, y in zip(a[:2], b[:2]):
         for u, v in x.items():
             for p, q in zip(v[1:], y[u][1:]):

@@ -205,7 +205,8 @@ def test_c5_subproblem_is_the_diagonal_subtree(depth):
     assert _rel_blocks(b, 0) == _rel_blocks(node, node.row.indices.first)
 
 
-NATIVE_VARIANTS = [("std", False), ("accu-combined", False), ("accu-merged", False)]
+NATIVE_VARIANTS = [("std", False), ("accu-combined", False), ("accu-merged", False),
+                   ("std", True), ("accu-merged", True)]
 
 
 @pytest.mark.parametrize("name", ["s1", "c1", "s2", "c4_0", "c2"])
@@ -220,14 +221,51 @@ def test_native_dags_match_reference(name):
     bt = BlockTable(broot)
     n = 0
     for mode, sp in NATIVE_VARIANTS:
-        if mode not in meta["dags"]:
+        tag = f"{mode}{'+sparsify' if sp else ''}"
+        if tag not in meta["dags"]:
             continue
-        ref = meta["dags"][mode]
-        g = tg.build_dag_native(bt, mode)
-        assert g.stats() == (ref["nodes"], ref["edges"]), mode
-        assert tg.canonical_hashes(g) == (ref["nodes_sha"], ref["edges_sha"]), mode
+        ref = meta["dags"][tag]
+        g = tg.build_dag_native(bt, mode, sparsify=sp)
+        assert g.stats() == (ref["nodes"], ref["edges"]), tag
+        assert tg.canonical_hashes(g) == (ref["nodes_sha"], ref["edges_sha"]), tag
         n += 1
     assert n >= 2
+
+
+@pytest.mark.parametrize("op", ["hlu", "hmul", "htrsl", "htrsu"])
+@pytest.mark.parametrize("cap", [1, 2, 3])
+def test_native_sparsify_equals_python(op, cap):
+    """Native per-round sparsification (hmx_dag_build_ex) vs the Python
+    builder's (itself pinned to the reference's std+sparsify and
+    accu-merged+sparsify hashes above) at path caps 1-3, for every root op."""
+    cfg = configs.config("s2")
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    for mode in ("std", "accu-merged") if op == "hlu" else ("std",):
+        if op == "hlu":
+            g1 = tg.build_hlu_dag(bt, mode, sparsify=True, max_path_len=cap)
+        else:
+            r, b = tg.root_task(bt, mode, op)
+            g1 = tg.compute_dag(r, mode=mode, table=bt, _builder=b, sparsify=True, max_path_len=cap)
+        g2 = tg.build_dag_native(bt, mode, op=op, sparsify=True, max_path_len=cap)
+        assert g1.stats() == g2.stats(), (mode, cap)
+        assert tg.canonical_hashes(g1) == tg.canonical_hashes(g2), (mode, cap)
+        if cap == 1:  # no path of length >= 2 is searched: nothing removed
+            assert g2.stats() == tg.build_dag_native(bt, mode, op=op).stats()
+
+
+def test_native_sparsify_errors_and_closure():
+    cfg = configs.config("s1")
+    _, _, _, broot = configs.structure(cfg)
+    bt = BlockTable(broot)
+    with pytest.raises(ValueError):
+        tg.build_dag_native(bt, "accu-combined", sparsify=True)
+    with pytest.raises(ValueError):
+        tg.build_dag_native(bt, "std", sparsify=True, max_path_len=0)
+    g0 = tg.build_dag_native(bt, "std")
+    g1 = tg.build_dag_native(bt, "std", sparsify=True)
+    assert g1.n_edges < g0.n_edges
+    assert tg.transitive_closure(g0) == tg.transitive_closure(g1)
 
 
 @pytest.mark.parametrize("op", ["hmul", "htrsl", "htrsu"])
