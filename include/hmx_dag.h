@@ -49,6 +49,12 @@ int64_t hmx_dag_edges(const hmx_dag* dag);
 int hmx_dag_export(const hmx_dag* dag, int32_t* kind, int32_t* nm, int32_t* mids, int32_t* nu,
                    int32_t* uids, double* alpha, int64_t* succ_ptr, int32_t* succ_idx);
 void hmx_dag_free(hmx_dag* dag);
+/* ASAP wavefronts ("levels") of any CSR graph with n nodes (ptr n+1, idx
+ * ptr[n]): level[v] = longest path length from a source to v; the wave
+ * schedule of the executors (engine.ExecPlan) and taskgraph.asap_levels.
+ * Returns 0; 1 bad argument; 3 cyclic graph (the reference's CycleError,
+ * taskgraph.py:440-441). */
+int hmx_dag_levels(int64_t n, const int64_t* succ_ptr, const int32_t* succ_idx, int32_t* level);
 
 #ifdef __cplusplus
 }

@@ -518,4 +518,33 @@ int hmx_dag_export(const hmx_dag* d, int32_t* kind, int32_t* nm, int32_t* mids, 
 
 void hmx_dag_free(hmx_dag* d) { delete d; }
 
+// ASAP wavefront of every node of a CSR graph (Kahn): level[v] = length of
+// the longest path from a source to v.  Returns 0, 1 bad argument, 3 cycle.
+int hmx_dag_levels(int64_t n, const int64_t* ptr, const int32_t* idx, int32_t* level) {
+  if (n < 0 || (n > 0 && (!ptr || !level))) return 1;
+  const int64_t ne = n ? ptr[n] : 0;
+  for (int64_t e = 0; e < ne; ++e)
+    if (idx[e] < 0 || idx[e] >= n) return 1;
+  std::vector<int32_t> indeg((size_t)n, 0), ready, nxt;
+  for (int64_t e = 0; e < ne; ++e) indeg[idx[e]]++;
+  for (int64_t i = 0; i < n; ++i) {
+    level[i] = 0;
+    if (!indeg[i]) ready.push_back((int32_t)i);
+  }
+  int64_t seen = 0;
+  while (!ready.empty()) {
+    nxt.clear();
+    for (int32_t u : ready) {
+      ++seen;
+      for (int64_t e = ptr[u]; e < ptr[u + 1]; ++e) {
+        const int32_t v = idx[e];
+        level[v] = std::max(level[v], level[u] + 1);
+        if (--indeg[v] == 0) nxt.push_back(v);
+      }
+    }
+    ready.swap(nxt);
+  }
+  return seen == n ? 0 : 3;
+}
+
 }  // extern "C"

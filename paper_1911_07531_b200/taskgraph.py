@@ -411,7 +411,32 @@ class TaskGraph:
 
 
 def asap_levels(n, ptr, idx, extra_edges=None):
-    """ASAP wavefront index of every node (Kahn's algorithm)."""
+    """ASAP wavefront index of every node (Kahn's algorithm, native
+    hmx_dag_levels)."""
+    import ctypes as C
+
+    ptr = np.asarray(ptr, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int32)
+    if extra_edges is not None and len(extra_edges):
+        ex = np.asarray(list(extra_edges), dtype=np.int64).reshape(-1, 2)
+        src = np.concatenate([np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr)), ex[:, 0]])
+        dst = np.concatenate([idx.astype(np.int64), ex[:, 1]])
+        o = np.argsort(src, kind="stable")
+        idx = dst[o].astype(np.int32)
+        ptr = np.concatenate([[0], np.cumsum(np.bincount(src, minlength=n))]).astype(np.int64)
+    ptr = np.ascontiguousarray(ptr)
+    idx = np.ascontiguousarray(idx) if len(idx) else np.zeros(1, np.int32)
+    level = np.empty(max(n, 1), dtype=np.int32)
+    rc = _native().hmx_dag_levels(int(n), ptr.ctypes.data, idx.ctypes.data, level.ctypes.data)
+    if rc == 3:
+        raise CycleError("cyclic execution graph")
+    if rc:
+        raise ValueError(f"hmx_dag_levels failed ({rc})")
+    return level[:n]
+
+
+def asap_levels_py(n, ptr, idx, extra_edges=None):
+    """Pure-Python restatement of asap_levels (test cross-check)."""
     succ = [idx[ptr[i]:ptr[i + 1]].tolist() for i in range(n)]
     if extra_edges is not None:
         for a, b in extra_edges:
@@ -712,6 +737,8 @@ def _native():
         L.hmx_dag_export.restype = C.c_int
         L.hmx_dag_free.argtypes = [vp]
         L.hmx_dag_free.restype = None
+        L.hmx_dag_levels.argtypes = [i64, vp, vp, vp]
+        L.hmx_dag_levels.restype = C.c_int
         _dag_lib = L
     return _dag_lib
 

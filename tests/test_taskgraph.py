@@ -107,6 +107,28 @@ def test_levels_and_csr():
             assert lv[j] > lv[i]
 
 
+def test_native_levels_equal_python():
+    """hmx_dag_levels (native wavefronts) = the Python Kahn restatement, with
+    and without extra edges; a cycle raises CycleError."""
+    import numpy as np
+
+    cfg = configs.config("s2")
+    _, _, _, broot = configs.structure(cfg)
+    for mode in ("std", "accu-merged"):
+        g = tg.build_dag_native(BlockTable(broot), mode, sparsify=mode == "std")
+        ptr, idx = g.csr()
+        extra = [(0, g.n_nodes - 1), (1, g.n_nodes - 2)]
+        for ex in (None, extra):
+            a = tg.asap_levels(g.n_nodes, ptr, idx, ex)
+            b = tg.asap_levels_py(g.n_nodes, ptr, idx, ex)
+            assert np.array_equal(a, b)
+    ptr = np.array([0, 1, 2], np.int32)
+    idx = np.array([1, 0], np.int32)
+    with pytest.raises(tg.CycleError):
+        tg.asap_levels(2, ptr, idx)
+    assert len(tg.asap_levels(0, np.zeros(1, np.int32), np.zeros(0, np.int32))) == 0
+
+
 @pytest.mark.parametrize("name", ["c3s", "c5s"])
 def test_large_trees_match_reference(name):
     """Configs 3 and 5: cluster tree, permutation and block tree bit-exact."""
