@@ -919,27 +919,25 @@ class Planner:
         self.ops = flat
         n = len(self.ops)
         arr = np.zeros(n, dtype=L.OP_DTYPE)
-        code = np.empty(n, np.int32)
-        flags = np.empty(n, np.int32)
-        dims = np.empty((n, 4), np.int32)
-        lds = np.empty((n, 4), np.int32)
-        refs = np.empty((n, 4), np.int64)
-        slots = np.empty((n, 4), np.int32)
-        iargs = np.empty((n, 4), np.int32)
-        fargs = np.empty((n, 2), np.float64)
-        wref = np.empty(n, np.int64)
-        for i, (c, f, d, l, r, s, ia, fa, w) in enumerate(self.ops):
-            code[i] = c
-            flags[i] = f
-            dims[i] = [iv(x) for x in d]
-            lds[i] = l
-            refs[i] = [rv(x) for x in r]
-            slots[i] = s
-            iargs[i] = [iv(x) for x in ia]
-            fargs[i] = fa
-            wref[i] = rv(w)
-        arr["code"], arr["flags"], arr["dim"], arr["ld"] = code, flags, dims, lds
-        arr["ref"], arr["slot"], arr["iarg"], arr["farg"], arr["wref"] = refs, slots, iargs, fargs, wref
+        # columns are gathered as Python lists and converted once (per-row
+        # numpy assignment dominated the planning time); lazy dimensions
+        # and refs are resolved here, plain ints pass through
+        _int = int
+
+        def ivs(t):
+            return [x if type(x) is _int else iv(x) for x in t]
+
+        if n:
+            code, flags, dims, lds, refs, slots, iargs, fargs, wrefs = zip(*self.ops)
+            arr["code"] = np.asarray(code, np.int32)
+            arr["flags"] = np.asarray(flags, np.int32)
+            arr["dim"] = np.asarray([ivs(d) for d in dims], np.int32).reshape(n, 4)
+            arr["ld"] = np.asarray(lds, np.int32).reshape(n, 4)
+            arr["ref"] = np.asarray([[rv(x) for x in r] for r in refs], np.int64).reshape(n, 4)
+            arr["slot"] = np.asarray(slots, np.int32).reshape(n, 4)
+            arr["iarg"] = np.asarray([ivs(a) for a in iargs], np.int32).reshape(n, 4)
+            arr["farg"] = np.asarray(fargs, np.float64).reshape(n, 2)
+            arr["wref"] = np.asarray([rv(w) for w in wrefs], np.int64)
         prog.ops = arr
         prog.task_ops = np.asarray(starts + [n], dtype=np.int64)
         prog.keys = [self.keys[t] for t in order]
