@@ -21,7 +21,18 @@
 #define HMX_JROT 0
 #endif
 #ifndef HMX_GSMALL
-#define HMX_GSMALL 0
+#define HMX_GSMALL 1
+#endif
+// unroll factor of the GEMM k-loop (loads of several k steps in flight)
+#ifndef HMX_GUNROLL
+#define HMX_GUNROLL 1
+#endif
+#define HMX_PRAGMA_(x) _Pragma(#x)
+#define HMX_PRAGMA(x) HMX_PRAGMA_(x)
+#if HMX_GUNROLL > 1
+#define HMX_GEMM_UNROLL HMX_PRAGMA(unroll HMX_GUNROLL)
+#else
+#define HMX_GEMM_UNROLL
 #endif
 #ifndef HMX_RRQR_THR
 #define HMX_RRQR_THR 1e-4
@@ -171,6 +182,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
       const double* As = sm + (c & 1) * (SA + SB);
       const double* Bs = As + SA;
       const int kc = min(KC, k - c * KC);
+      HMX_GEMM_UNROLL
       for (int kk = 0; kk < kc; ++kk) {
         double a[MI], b[MJ];
 #pragma unroll
