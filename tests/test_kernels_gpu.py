@@ -77,6 +77,28 @@ def test_gemm(ta, tb):
         assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
 
 
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_gemm_small_path_bitwise_equals_tiled(ta, tb):
+    """The small-output GEMM (m*n <= 4*threads, one-pass staging) and the
+    64x64 tiled GEMM run the same increasing-k fma chain per output: a
+    sub-block computed alone (small path) equals the same entries of a large
+    product (tiled path) bit for bit."""
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(11)
+    m, n, k = 96, 80, 45
+    A = rng.normal(size=(k, m) if ta else (m, k))
+    B = rng.normal(size=(n, k) if tb else (k, n))
+    C0 = rng.normal(size=(m, n))
+    big = kernels.gemm(-0.7, [A], [B], [C0], transA=ta, transB=tb, beta=1.0)[0]
+    for (i0, i1, j0, j1) in ((0, 16, 0, 16), (5, 37, 3, 20), (90, 96, 0, 80)):
+        As = A[:, i0:i1] if ta else A[i0:i1, :]
+        Bs = B[j0:j1, :] if tb else B[:, j0:j1]
+        sub = kernels.gemm(-0.7, [np.ascontiguousarray(As)], [np.ascontiguousarray(Bs)],
+                           [np.ascontiguousarray(C0[i0:i1, j0:j1])], transA=ta, transB=tb, beta=1.0)[0]
+        assert np.array_equal(sub, big[i0:i1, j0:j1])
+
+
 class _Pol:
     def __init__(self, mode, eps=None, k=None):
         self.mode, self.eps, self.k = mode, eps, k
