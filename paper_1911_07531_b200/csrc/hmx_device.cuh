@@ -23,16 +23,6 @@
 #ifndef HMX_GSMALL
 #define HMX_GSMALL 1
 #endif
-// loads in flight per thread in the elementwise copy/add/append loops (0 =
-// the plain one-element-at-a-time loop)
-#ifndef HMX_CBATCH
-#define HMX_CBATCH 0
-#endif
-#if HMX_CBATCH
-#define HMX_CB_FN __device__ __noinline__  // out of line: no register pressure on the interpreter
-#else
-#define HMX_CB_FN __device__
-#endif
 // unroll factor of the GEMM k-loop (loads of several k steps in flight)
 #ifndef HMX_GUNROLL
 #define HMX_GUNROLL 2
@@ -93,70 +83,19 @@ __device__ void cta_zero(int m, int n, double* C, int ldc) {
   FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] = 0.0;
 }
 
-#if HMX_CBATCH
-// Elementwise m x n map with the loads batched: a warp owns units of 32 rows
-// of one column (lanes over rows, coalesced) and every thread issues the
-// loads of HMX_CBATCH units before any of their stores.  The plain FOR_MN
-// loop serialises one global load -> store round trip per element (source
-// and destination may alias as far as the compiler knows); here each
-// element is still read and written exactly once by one thread, with the
-// same arithmetic, so the results are bitwise identical.
-template <class Ld, class St>
-__device__ __forceinline__ void cta_map_batched(int m, int n, Ld ld, St st) {
-  constexpr int B = HMX_CBATCH;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int rch = (m + 31) >> 5;
-  const int total = rch * n;
-  for (int u0 = w; u0 < total; u0 += HMX_WARPS * B) {
-    double v[B];
-    int ii[B], jj[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const int u = u0 + b * HMX_WARPS;
-      const int j = u / rch;
-      const int i = ((u - j * rch) << 5) + lane;
-      ii[b] = (u < total && i < m) ? i : -1;
-      jj[b] = j;
-      if (ii[b] >= 0) v[b] = ld(i, j);
-    }
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (ii[b] >= 0) st(ii[b], jj[b], v[b]);
-  }
-}
-#endif
 
 // C (m x n) = alpha * op(A); transA: A is n x m.
-HMX_CB_FN void cta_copy(int m, int n, double alpha, const double* A, int lda, bool ta, double* C,
-                       int ldc) {
-#if HMX_CBATCH
-  if (!ta) {
-    cta_map_batched(m, n, [&](int i, int j) { return alpha * A[i + (int64_t)j * lda]; },
-                    [&](int i, int j, double x) { C[i + (int64_t)j * ldc] = x; });
-  } else {
-    // transposed source: iterate over A's columns (coalesced reads)
-    cta_map_batched(n, m, [&](int j, int i) { return alpha * A[j + (int64_t)i * lda]; },
-                    [&](int j, int i, double x) { C[i + (int64_t)j * ldc] = x; });
-  }
-#else
+__device__ void cta_copy(int m, int n, double alpha, const double* A, int lda, bool ta, double* C,
+                         int ldc) {
   if (!ta) {
     FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] = alpha * A[i + (int64_t)j * lda];
   } else {
     FOR_MN(j, i, n, m) C[i + (int64_t)j * ldc] = alpha * A[j + (int64_t)i * lda];
   }
-#endif
 }
 
-HMX_CB_FN void cta_add(int m, int n, double alpha, const double* A, int lda, double* C, int ldc) {
-#if HMX_CBATCH
-  cta_map_batched(m, n,
-                  [&](int i, int j) {
-                    return C[i + (int64_t)j * ldc] + alpha * A[i + (int64_t)j * lda];
-                  },
-                  [&](int i, int j, double x) { C[i + (int64_t)j * ldc] = x; });
-#else
+__device__ void cta_add(int m, int n, double alpha, const double* A, int lda, double* C, int ldc) {
   FOR_MN(i, j, m, n) C[i + (int64_t)j * ldc] += alpha * A[i + (int64_t)j * lda];
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -268,7 +207,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
         for (int i = 0; i < MI; ++i) {
           const int gi = m0 + tr + 16 * i;
           const double cv = (gi < m && gj < n) ? C[gi + (int64_t)gj * ldc] : 0.0;
-          acc[i][j] = cv + alpha * acc[i][j];
+          acc[i][j] = fma(alpha, acc[i][j], cv);  // explicit: every GEMM path rounds alike
         }
       }
     } else {
@@ -420,7 +359,7 @@ __device__ __noinline__ void gemm_small(int m, int n, int k, double alpha, const
   for (int r = 0; r < 4; ++r) {
     const int e = tid + r * HMX_THREADS;
     if (e < mn) {
-      const double o = beta1 ? cv[r] + alpha * acc[r] : alpha * acc[r];
+      const double o = beta1 ? fma(alpha, acc[r], cv[r]) : alpha * acc[r];
       C[ii[r] + (int64_t)(jj[r] / kb) * ldc] = o;
     }
   }

@@ -456,18 +456,6 @@ __device__ void op_svals(const DevPlan& P, const Cx& c, const hmx_op& o, double*
 // ---------------------------------------------------------------------------
 // one op
 // ---------------------------------------------------------------------------
-#if HMX_CBATCH
-// APPEND's column copy: dst rows [r0, r0 + mq) from src, the rest zero
-__device__ __noinline__ void append_cols(int M, int k, int r0, int mq, const double* S, int lds,
-                                         double* D, int ldd) {
-  cta_map_batched(M, k,
-                  [&](int i, int t) {
-                    return (i >= r0 && i < r0 + mq) ? S[(i - r0) + (int64_t)t * lds] : 0.0;
-                  },
-                  [&](int i, int t, double x) { D[i + (int64_t)t * ldd] = x; });
-}
-#endif
-
 __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
   double* red = sm;
   double* work = sm + 32;
@@ -605,17 +593,12 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       const double* Vs = mref(P, c, o.ref[1]);
       double* Ud = mref(P, c, o.ref[2]) + (int64_t)col0 * o.ld[2];
       double* Vd = mref(P, c, o.ref[3]) + (int64_t)col0 * o.ld[3];
-#if HMX_CBATCH
-      append_cols(M, k, r0, mq, Us, o.ld[0], Ud, o.ld[2]);
-      append_cols(N, k, c0, nq, Vs, o.ld[1], Vd, o.ld[3]);
-#else
       FOR_MN(i, t, M, k)
         Ud[i + (int64_t)t * o.ld[2]] =
             (i >= r0 && i < r0 + mq) ? Us[(i - r0) + (int64_t)t * o.ld[0]] : 0.0;
       FOR_MN(i, t, N, k)
         Vd[i + (int64_t)t * o.ld[3]] =
             (i >= c0 && i < c0 + nq) ? Vs[(i - c0) + (int64_t)t * o.ld[1]] : 0.0;
-#endif
       __syncthreads();
       if (threadIdx.x == 0) *cnt = col0 + k;
       __syncthreads();
