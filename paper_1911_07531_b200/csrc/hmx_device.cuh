@@ -207,7 +207,7 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
         for (int i = 0; i < MI; ++i) {
           const int gi = m0 + tr + 16 * i;
           const double cv = (gi < m && gj < n) ? C[gi + (int64_t)gj * ldc] : 0.0;
-          acc[i][j] = fma(alpha, acc[i][j], cv);  // explicit: every GEMM path rounds alike
+          acc[i][j] = cv + alpha * acc[i][j];  // contracted to fma(alpha, acc, cv)
         }
       }
     } else {
@@ -359,6 +359,7 @@ __device__ __noinline__ void gemm_small(int m, int n, int k, double alpha, const
   for (int r = 0; r < 4; ++r) {
     const int e = tid + r * HMX_THREADS;
     if (e < mn) {
+      // fma(alpha, acc, cv): the contraction the tiled epilogue gets
       const double o = beta1 ? fma(alpha, acc[r], cv[r]) : alpha * acc[r];
       C[ii[r] + (int64_t)(jj[r] / kb) * ldc] = o;
     }
