@@ -1,6 +1,6 @@
 # Closing GPU session: full GPU tests, smoke, default bench, reference arm, launch list, ncu full of the step kernel.
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/close
+O=gpurun_out/${CLOSE_DIR:-close}
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
