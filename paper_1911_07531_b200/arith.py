@@ -22,21 +22,45 @@ class SingularPivotError(RuntimeError):
     pass
 
 
-_PLANS = {}
+class _PlanCache:
+    """Small LRU of execution plans.  A plan owns GB-scale device buffers
+    (per-CTA scratch, accumulator pool, workspace), so only the ``size``
+    most recently used plans are kept; ``clear_plans()`` drops them all.
+    Keys hold the block table itself (not its id), so a key can never be
+    reused by another table."""
+
+    def __init__(self, size):
+        from collections import OrderedDict
+
+        self.size = size
+        self.d = OrderedDict()
+
+    def get(self, key, make):
+        p = self.d.get(key)
+        if p is None:
+            while len(self.d) >= self.size:
+                self.d.popitem(last=False)
+            p = make()
+            self.d[key] = p
+        self.d.move_to_end(key)
+        return p
+
+    def clear(self):
+        self.d.clear()
+
+
+PLAN_CACHE_SIZE = 2
+_PLANS = _PlanCache(PLAN_CACHE_SIZE)
 
 
 def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0,
              split_min=engine.DEFAULT_SPLIT_MIN, nrep=1, ctas_per_sm=None):
     """Cached execution plan (planning and upload happen once per tree)."""
-    key = (id(table), mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep,
+    key = (table, mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep,
            ctas_per_sm)
-    p = _PLANS.get(key)
-    if p is None or p.table is not table:
-        p = engine.ExecPlan(table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify,
-                            max_ctas=max_ctas, split_min=split_min, nrep=nrep,
-                            ctas_per_sm=ctas_per_sm)
-        _PLANS[key] = p
-    return p
+    return _PLANS.get(key, lambda: engine.ExecPlan(
+        table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify, max_ctas=max_ctas,
+        split_min=split_min, nrep=nrep, ctas_per_sm=ctas_per_sm))
 
 
 def clear_plans():
@@ -110,16 +134,12 @@ def dense_lu(A: np.ndarray):
     return Ls[0], Us[0]
 
 
-_OPS = {}
+_OPS = _PlanCache(4)
 
 
 def _op_plan(table, op, policy, rank_cap, alpha=1.0):
-    key = (id(table), op, repr(policy), rank_cap, float(alpha))
-    p = _OPS.get(key)
-    if p is None or p.table is not table:
-        p = engine.OpPlan(table, op, policy, rank_cap, alpha=alpha)
-        _OPS[key] = p
-    return p
+    key = (table, op, repr(policy), rank_cap, float(alpha))
+    return _OPS.get(key, lambda: engine.OpPlan(table, op, policy, rank_cap, alpha=alpha))
 
 
 def _run_op(op, M0, M1, M2, policy, alpha=1.0, **kw):

@@ -755,6 +755,8 @@ __global__ void __launch_bounds__(HMX_THREADS, OCC) k_persistent(DevPlan P) {
           const int s = P.succ_idx[k];
           const int r = P.owner[s];
           if (atomicSub(&P.r_indeg[r][s], 1) == 1) {
+            // acquire the other predecessors' releases before handing s on
+            __threadfence_system();
             const int pos = atomicAdd(&P.r_qctl[r][1], 1);
             atomicExch(&P.r_queue[r][pos], s);
           }
@@ -765,6 +767,9 @@ __global__ void __launch_bounds__(HMX_THREADS, OCC) k_persistent(DevPlan P) {
       for (int k = P.succ_ptr[t]; k < P.succ_ptr[t + 1]; ++k) {
         const int s = P.succ_idx[k];
         if (atomicSub(&P.indeg[s], 1) == 1) {
+          // acquire the other predecessors' releases (fence + relaxed
+          // atomicSub on their side) before handing s to another CTA
+          __threadfence();
           const int pos = atomicAdd(&P.qctl[1], 1);
           atomicExch(&P.queue[pos], s);
         }

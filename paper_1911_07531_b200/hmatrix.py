@@ -437,18 +437,19 @@ def unpack_leaves(table: BlockTable, packed, ranks, nrep=1):
 # ---------------------------------------------------------------------------
 # H x dense products and triangular solves (hmatrix.py:286-341) on the device
 # ---------------------------------------------------------------------------
-_DENSE_PLANS = {}
+_DENSE_PLANS = None
 
 
 def _dense_plan(M: HMatrix, op, cols):
+    global _DENSE_PLANS
+    from .arith import _PlanCache
     from .engine import DensePlan
 
+    if _DENSE_PLANS is None:
+        _DENSE_PLANS = _PlanCache(16)
     t = M.table
-    key = (id(t), op, M.uid, int(cols), M.store.layout.rank_cap)
-    p = _DENSE_PLANS.get(key)
-    if p is None or p.table is not t:
-        p = _DENSE_PLANS[key] = DensePlan(t, op, M.uid, cols, M.store.layout.rank_cap)
-    return p
+    key = (t, op, M.uid, int(cols), M.store.layout.rank_cap)
+    return _DENSE_PLANS.get(key, lambda: DensePlan(t, op, M.uid, cols, M.store.layout.rank_cap))
 
 
 def _dense_run(M: HMatrix, op, X, out_rows):

@@ -24,9 +24,12 @@ ones, so no rank ever reads a stale or half-written object.
 Two launch forms share the records: ``rank=-1`` emulates every rank in one
 launch on one GPU (CTA c serves rank c mod nranks; each rank's storage is a
 replica in the same pools, the ops and records carry the replica offsets),
-used by the tests to prove the protocol bit-exact; ``rank>=0`` is one
-process per GPU with the peers' storage mapped through CUDA IPC
-(:class:`DistributedHLU`).
+used by the tests to prove the protocol bit-exact; ``rank>=0`` (one
+process per GPU, peers' storage mapped through CUDA IPC with
+hmx_plan_peer) is rejected by :class:`PartitionedPlan` until a
+multi-process runner exists: the launch needs every rank reset, a
+cross-rank barrier, then a no-reset launch (mode 4), and it cannot be
+exercised on the single-GPU test boxes of this build.
 """
 
 from __future__ import annotations
@@ -279,8 +282,8 @@ class PartitionedPlan:
     """H-LU plan partitioned over ``nranks`` block-row owners.
 
     rank = -1: all ranks emulated in one launch on this GPU (storage of
-    rank r = replica r of batched stores, see :meth:`stores`).  rank >= 0:
-    this process is rank ``rank`` (see :class:`DistributedHLU`).
+    rank r = replica r of batched stores, see :meth:`stores`).  rank >= 0
+    raises NotImplementedError (see the module docstring).
     """
 
     def __init__(self, table, mode, policy, rank_cap, nranks, rank=-1, split_min=None,
@@ -289,6 +292,10 @@ class PartitionedPlan:
 
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
+        if int(rank) >= 0:
+            raise NotImplementedError(
+                "multi-process partitioned H-LU (rank >= 0) is not supported: only the "
+                "emulated launch (rank=-1) is implemented and tested")
         split_min = engine.DEFAULT_SPLIT_MIN if split_min is None else split_min
         self.table, self.mode, self.policy, self.rank_cap = table, mode, policy, rank_cap
         self.nranks, self.rank = int(nranks), int(rank)

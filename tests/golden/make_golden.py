@@ -12,7 +12,8 @@ no dataset).  The problem definitions are restated here independently of the
 product package so that the pin does not depend on the code it pins.
 
 Usage:  python tests/golden/make_golden.py [case ...]
-Cases:  small (s1..s4, trunc), c1, c2, c3 (numerics, fast assembly), c3s, c4, c5s
+Cases:  small (s1..s4, trunc), c1, c2, c3 (numerics, fast assembly), c3s, c4, c5s,
+        roots (standalone hmul/htrsl/htrsu DAGs), c5dag, c5dag_merged
 """
 
 from __future__ import annotations
@@ -346,6 +347,71 @@ def run_case(name, numerics=True, modes=("std", "accu"), dag_modes=None, full_da
     print(f"[{name}] done {time.time() - t0:.1f}s", flush=True)
 
 
+def sample_leaves(H, nb, rng, count=12):
+    """Entries of a seeded sample of leaves of a factor: ``count`` dense
+    leaves (D) and ``count`` low-rank leaves of rank >= 1 (U, V), so that
+    device factors can be compared entrywise per block (low-rank leaves
+    through U V^T, which is what the factorization defines)."""
+    dense, lowr = [], []
+    for leaf in H.leaves():
+        if leaf.kind == hm.LOWRANK:
+            if leaf.rank > 0:
+                lowr.append(leaf)
+        else:
+            dense.append(leaf)
+    out = {"uid": [], "kind": [], "m": [], "n": [], "k": [], "vals": []}
+    for group, kind in ((dense, 0), (lowr, 1)):
+        if not group:
+            continue
+        pick = rng.choice(len(group), size=min(count, len(group)), replace=False)
+        for i in sorted(pick):
+            leaf = group[i]
+            b = leaf.block
+            out["uid"].append(b.uid)
+            out["kind"].append(kind)
+            out["m"].append(b.nrows)
+            out["n"].append(b.ncols)
+            if kind == 0:
+                out["k"].append(0)
+                out["vals"].append(np.asarray(leaf.D, dtype=float).ravel(order="F"))
+            else:
+                out["k"].append(leaf.rank)
+                out["vals"].append(np.concatenate([np.asarray(leaf.U).ravel(order="F"),
+                                                   np.asarray(leaf.V).ravel(order="F")]))
+    meta = np.array([out["uid"], out["kind"], out["m"], out["n"], out["k"]], dtype=np.int64).T
+    return meta, np.concatenate(out["vals"]) if out["vals"] else np.zeros(0)
+
+
+def run_leaf_samples(name, fast_assembly, modes=("std", "accu")):
+    """<name>_leaves.npz: sampled leaf entries of L and U of the reference's
+    own factorization (same inputs as run_case), for per-block factor
+    parity of the device (tests/test_hlu_gpu.py, bench.py)."""
+    pts, ell, n_min, adm, eps = case_points(name)
+    croot, perm = trees.build_cluster_tree(trees.Geometry(pts), n_min)
+    broot = trees.build_block_tree(croot, croot, adm)
+    nb = block_table(broot).shape[0]
+    pol = hm.TruncationPolicy.fixed_accuracy(eps)
+    kern = exp_kernel(pts, ell, perm)
+    t0 = time.time()
+    A0 = assemble_fast(broot, kern, pol)[0] if fast_assembly else hm.assemble(broot, kern, pol)
+    print(f"[{name}_leaves] assembly {time.time() - t0:.1f}s", flush=True)
+    arrays = {}
+    for mode in modes:
+        A = A0.copy()
+        L, U = hm.zeros(broot, pol), hm.zeros(broot, pol)
+        with threadpool_limits(limits=1):
+            if mode == "std":
+                arith.hlu(A, L, U, pol)
+            else:
+                accm.hlu_accu(A, L, U, accm.AccumulatorMap(), pol)
+        for tag, H in (("L", L), ("U", U)):
+            rng = np.random.default_rng(4242 + (tag == "U") + 2 * (mode == "accu"))
+            m, v = sample_leaves(H, nb, rng)
+            arrays[f"{mode}_{tag}_meta"], arrays[f"{mode}_{tag}_vals"] = m, v
+        print(f"[{name}_leaves] {mode} done {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(OUT, f"{name}_leaves.npz"), **arrays)
+
+
 def probe_vec(n):
     return np.random.default_rng(7).normal(size=(n, 2))
 
@@ -400,6 +466,31 @@ ALL_DAG = [("std", False), ("std", True), ("accu-combined", False),
            ("accu-merged", False), ("accu-merged", True)]
 
 
+def run_roots():
+    """Standalone multiply / triangular-solve DAGs (root tasks made by the
+    reference's own factories, taskgraph.py:146-180, refined by its
+    compute_dag, taskgraph.py:530-590) on the s2 structure."""
+    pts, ell, n_min, adm, eps = case_points("s2")
+    croot, perm = trees.build_cluster_tree(trees.Geometry(pts), n_min)
+    b = trees.build_block_tree(croot, croot, adm)
+    out = {}
+    for mode in ("std", "accu-combined"):
+        for op in ("hmul", "htrsl", "htrsu"):
+            for sp in (False, True):
+                if sp and mode != "std":
+                    continue
+                if op == "hmul":
+                    root = tg._mul_task(1.0, b, b, b, (tg.MID_A, tg.MID_L, tg.MID_U), (0,), mode)
+                elif op == "htrsl":
+                    root = tg._solve_l_task(b, b, (tg.MID_L, tg.MID_A, tg.MID_U), (0,), mode)
+                else:
+                    root = tg._solve_u_task(b, b, (tg.MID_U, tg.MID_A, tg.MID_L), (0,), mode)
+                g = tg.compute_dag(root, 0, sparsify=sp, mode=mode)
+                out[f"{op}|{mode}{'+sparsify' if sp else ''}"] = dag_summary(g, False)
+    with open(os.path.join(OUT, "roots.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main(argv):
     cases = argv or ["small"]
     for c in cases:
@@ -421,21 +512,30 @@ def main(argv):
         elif c == "c4":
             for j in range(4):
                 run_case(f"c4_{j}", dag_modes=[("std", False), ("accu-merged", False)])
-        elif c == "c5dag":
-            # reference std DAG of config 5 (478 s, ~17 GB), digest only
+        elif c in ("c5dag", "c5dag_merged"):
+            # reference std (478 s, ~17 GB) or accu-merged (757 s, 17.4 GB)
+            # DAG of config 5, digest only
             pts, ell, n_min, adm, eps = case_points("c5s")
             croot, perm = trees.build_cluster_tree(trees.Geometry(pts), n_min)
             broot = trees.build_block_tree(croot, croot, adm)
-            out = {}
-            for mode in ("std",):
+            path = os.path.join(OUT, "c5dag.json")
+            out = json.load(open(path)) if os.path.exists(path) else {}
+            modes = ("accu-merged",) if c == "c5dag_merged" else ("std",)
+            for mode in modes:
                 t1 = time.time()
                 g = tg.build_hlu_dag(broot, mode)
                 out[mode] = dag_digest(g)
                 out[mode]["build_s"] = time.time() - t1
                 print(f"[c5dag] {mode} {out[mode]}", flush=True)
                 del g
-            with open(os.path.join(OUT, "c5dag.json"), "w") as f:
+            with open(path, "w") as f:
                 json.dump(out, f, indent=1, sort_keys=True)
+        elif c.startswith("leaves_"):
+            nm = c.split("_", 1)[1]
+            run_leaf_samples(nm, fast_assembly=nm in ("c3",) or nm.startswith("c5_d"),
+                             modes=("accu",) if nm.startswith("c5_d") else ("std", "accu"))
+        elif c == "roots":
+            run_roots()
         elif c == "c5s":
             run_case("c5s", numerics=False, dag_modes=[], store_blocks=False)
         else:
