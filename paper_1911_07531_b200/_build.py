@@ -67,12 +67,18 @@ def _run(cmd, log):
         raise RuntimeError("nvcc failed building libhmx.so")
 
 
+HOST_SOURCES = ["hmx_dag.cpp", "hmx_lower.cpp"]
+HOST_HEADERS = [os.path.join(ROOT, "include", h) for h in ("hmx.h", "hmx_dag.h", "hmx_lower.h")]
+
+
 def build_dag(force: bool = False) -> str:
-    """g++ -O2 -shared: the host-side refinement DAG builder."""
-    src = os.path.join(CSRC, "hmx_dag.cpp")
-    if force or not os.path.exists(DAG_LIB) or os.path.getmtime(src) > os.path.getmtime(DAG_LIB):
+    """g++ -O2 -shared: the host-side native runtime (refinement DAG builder
+    hmx_dag.cpp, H-LU lowering + execution graph hmx_lower.cpp)."""
+    srcs = [os.path.join(CSRC, s) for s in HOST_SOURCES]
+    newest = max(os.path.getmtime(p) for p in srcs + HOST_HEADERS)
+    if force or not os.path.exists(DAG_LIB) or newest > os.path.getmtime(DAG_LIB):
         res = subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall", "-o", DAG_LIB,
-                              src], capture_output=True, text=True)
+                              *srcs], capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)
             raise RuntimeError("g++ failed building libhmxdag.so")

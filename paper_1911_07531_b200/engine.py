@@ -211,33 +211,49 @@ class ExecPlan:
 
     def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
                  sparsify=False, max_ctas=0, nrep=1, split_min=DEFAULT_SPLIT_MIN,
-                 ctas_per_sm=None):
+                 ctas_per_sm=None, caps=None, python_planner=False, acc_budget=0, big_budget=None):
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
         self.table = table
         self.mode = mode
         self.policy = policy
         self.rank_cap = rank_cap
-        prog = plan_hlu(table, mode, policy, rank_cap, split_min=split_min)
-        self.prog = prog
-        self.layout = prog.layout
         dag_mode = dag_mode or ("std" if mode == "std" else tg.MERGED)
         if (mode == "std") != (dag_mode == tg.STD):
             raise ValueError(f"DAG mode {dag_mode} does not execute {mode} arithmetic")
-        if dag_mode == tg.COMBINED:
-            from .planner import fuse_applies
-
-            prog = fuse_applies(prog)
-            self.prog = prog
         self.dag_mode = dag_mode
-        # the reference DAG (sparsified or not): native builder (bit-exact,
-        # ~25x faster than the Python one)
-        self.dag = tg.build_dag_native(table, dag_mode, sparsify=sparsify)
-        ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()
+        if dag_mode != tg.COMBINED and not python_planner:
+            # native lowering + execution graph (csrc/hmx_lower.cpp) against
+            # the reference DAG from the native refinement builder
+            from .lower import NativeProgram
+
+            prog = NativeProgram(table, mode, policy, rank_cap, split_min=split_min, caps=caps,
+                                 acc_budget=acc_budget)
+            self.prog = prog
+            self.layout = prog.layout
+            h = tg.dag_handle(table, dag_mode, sparsify=sparsify)
+            ptr, idx = prog.graph(h.ptr, mode)
+            h.free()
+            self.n_dag_edges = prog.n_dag_edges
+            self.n_chain_edges = -1
+        else:
+            # Python planner (the specification of the native one) and, for
+            # the combined DAG, apply tasks fused into their leaf tasks
+            if caps is not None:
+                raise ValueError("rank-bounded layouts need the native planner")
+            prog = plan_hlu(table, mode, policy, rank_cap, split_min=split_min)
+            if dag_mode == tg.COMBINED:
+                from .planner import fuse_applies
+
+                prog = fuse_applies(prog)
+            self.prog = prog
+            self.layout = prog.layout
+            self.dag = tg.build_dag_native(table, dag_mode, sparsify=sparsify)
+            ptr, idx, self.n_dag_edges, self.n_chain_edges = self._exec_graph()
         self.succ_ptr, self.succ_idx = ptr, idx
-        lv = tg.asap_levels(len(prog.keys), ptr, idx)
+        lv = tg.asap_levels(len(prog.task_ops) - 1, ptr, idx)
         self.levels = lv
-        self.n_tasks = len(prog.keys)
+        self.n_tasks = len(prog.task_ops) - 1
         self.nrep = int(nrep)
         ops, task_ops = prog.ops, prog.task_ops
         if self.nrep > 1:

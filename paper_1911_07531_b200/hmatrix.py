@@ -237,16 +237,19 @@ def _store_cls():
     return HStore
 
 
-def _layout(table, rank_cap):
+def _layout(table, rank_cap, caps=None):
     from .planner import Layout
 
-    return Layout(table, rank_cap)
+    return Layout(table, rank_cap, caps)
 
 
-def zeros(block: Block, policy: TruncationPolicy = EXACT, rank_cap=DEFAULT_RANK_CAP) -> HMatrix:
-    """Zero H-matrix over a block tree (rank-0 admissible leaves, hmatrix.py:251-263)."""
+def zeros(block: Block, policy: TruncationPolicy = EXACT, rank_cap=DEFAULT_RANK_CAP,
+          caps=None) -> HMatrix:
+    """Zero H-matrix over a block tree (rank-0 admissible leaves, hmatrix.py:251-263).
+    ``caps``: optional per-uid bound of the low-rank arenas (rank-bounded
+    storage, assembly.rank_caps)."""
     t = table_of(block)
-    return HMatrix(_store_cls()(_layout(t, rank_cap)), block.uid, policy)
+    return HMatrix(_store_cls()(_layout(t, rank_cap, caps)), block.uid, policy)
 
 
 def from_leaves(block: Block, leaves, policy=EXACT, rank_cap=DEFAULT_RANK_CAP) -> HMatrix:
@@ -264,6 +267,25 @@ def assemble(block: Block, kernel, policy: TruncationPolicy, rank_cap=DEFAULT_RA
     store = _store_cls()(_layout(t, rank_cap))
     assemble_store(store, kernel, policy)
     return HMatrix(store, block.uid, policy)
+
+
+def assemble_bounded(block: Block, kernel, policy: TruncationPolicy, rank_cap=DEFAULT_RANK_CAP,
+                     mult=2.5, floor=24, budget=None):
+    """Rank-first assembly for large problems (config 5): leaves are
+    compressed chunk by chunk into the packed form, every low-rank arena is
+    then sized from the assembled rank (assembly.rank_caps) and A is
+    unpacked into that storage.  Returns (A, caps); factors of A must be
+    allocated with the same caps (``zeros(block, policy, rank_cap, caps)``)."""
+    from .assembly import DEFAULT_BUDGET, assemble_packed, rank_caps
+
+    t = table_of(block)
+    packed, ranks = assemble_packed(t, kernel, policy, rank_cap, budget or DEFAULT_BUDGET)
+    caps = rank_caps(t, ranks.cpu().numpy(), rank_cap, mult, floor)
+    store = _store_cls()(_layout(t, rank_cap, caps))
+    store.ranks.copy_(ranks)
+    store.unpack_from(packed)
+    del packed
+    return HMatrix(store, block.uid, policy), caps
 
 
 def rel_error(A, B) -> float:

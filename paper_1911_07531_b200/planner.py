@@ -48,10 +48,13 @@ def _al(n):
 class Layout:
     """Leaf storage offsets of an H-matrix over a block table."""
 
-    def __init__(self, table: BlockTable, rank_cap=None):
+    def __init__(self, table: BlockTable, rank_cap=None, caps=None):
+        """caps: optional per-uid capacity bound of low-rank leaves (-1 =
+        none), the rank-bounded arenas of large problems (hmx_lower.h)."""
         n = table.n
         self.table = table
         self.rank_cap = rank_cap
+        self.caps = caps
         self.d_off = np.full(n, -1, dtype=np.int64)
         self.u_off = np.full(n, -1, dtype=np.int64)
         self.v_off = np.full(n, -1, dtype=np.int64)
@@ -61,6 +64,8 @@ class Layout:
             m, nc = int(table.m[u]), int(table.nc[u])
             if table.adm[u]:
                 c = min(m, nc) if rank_cap is None else min(m, nc, int(rank_cap))
+                if caps is not None and caps[u] >= 0:
+                    c = min(c, int(caps[u]))
                 self.cap[u] = c
                 self.u_off[u] = cur
                 cur += _al(m * c)
@@ -70,6 +75,15 @@ class Layout:
                 self.d_off[u] = cur
                 cur += _al(m * nc)
         self.size = max(cur, 1)
+
+    @classmethod
+    def from_arrays(cls, table, rank_cap, d_off, u_off, v_off, cap, size):
+        """Layout computed elsewhere (native lowering, lower.py)."""
+        lay = cls.__new__(cls)
+        lay.table, lay.rank_cap, lay.caps = table, rank_cap, None
+        lay.d_off, lay.u_off, lay.v_off, lay.cap = d_off, u_off, v_off, cap
+        lay.size = max(int(size), 1)
+        return lay
 
     def same_as(self, other):
         return (self.table is other.table and self.rank_cap == other.rank_cap)

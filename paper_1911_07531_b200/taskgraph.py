@@ -465,6 +465,56 @@ def _native():
     return _dag_lib
 
 
+class DagHandle:
+    """Owned native DAG (hmx_dag*) for native consumers (lower.py); freed
+    with the object."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def n_nodes(self):
+        return int(_native().hmx_dag_nodes(self.ptr))
+
+    def n_edges(self):
+        return int(_native().hmx_dag_edges(self.ptr))
+
+    def free(self):
+        if self.ptr is not None:
+            _native().hmx_dag_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        self.free()
+
+
+def dag_handle(block_root, mode: str = STD, *, stop_size: int = 0, op: str = "hlu",
+               sparsify: bool = False, max_path_len: int = 2) -> DagHandle:
+    """The native build of build_dag_native, kept native (no export)."""
+    import ctypes as C
+
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if mode == COMBINED and sparsify:
+        raise ValueError("edge sparsification is not valid in combined accumulator mode")
+    t = _as_table(block_root)
+    L = _native()
+    arr = [np.ascontiguousarray(x, dtype=np.int64) for x in (t.r0, t.r1, t.c0, t.c1)]
+    leaf = np.ascontiguousarray(t.leaf, dtype=np.int8)
+    parent = np.ascontiguousarray(t.parent, dtype=np.int32)
+    kids = np.ascontiguousarray(np.where(t.kids < 0, -1, t.kids), dtype=np.int32).reshape(-1, 4)
+    h = C.c_void_p()
+    rc = L.hmx_dag_build_ex(t.n, *[a.ctypes.data for a in arr], leaf.ctypes.data, parent.ctypes.data,
+                            kids.ctypes.data, _MODE_CODE[mode], int(stop_size), _OP_CODE[op],
+                            int(bool(sparsify)), int(max_path_len), C.byref(h))
+    if rc == 2:
+        raise ValueError("structural error in refinement (leaf diagonal / operands)")
+    if rc == 3:
+        raise CycleError("refinement produced a cyclic graph")
+    if rc:
+        raise ValueError(f"hmx_dag_build failed ({rc})")
+    return DagHandle(h)
+
+
 def build_dag_native(block_root, mode: str = STD, *, stop_size: int = 0, op: str = "hlu",
                      sparsify: bool = False, max_path_len: int = 2):
     """Native (C++) refinement build; same node and edge sets as
