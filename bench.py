@@ -196,21 +196,29 @@ def parity_report(cfg, mode, L, U):
     Lr, Ur = L.store.ranks.cpu().numpy(), U.store.ranks.cpu().numpy()
     out["rank_mismatches"] = PT.compare_ranks(arr, mode, Lr, Ur)
     lay = L.store.layout
-    fro = []
+    rel, ab = [], []
     for which, M in (("L", L), ("U", U)):
         f = PT.store_fro(lay, M.store.values.cpu().numpy(), M.store.ranks.cpu().numpy())
-        fro.append(PT.compare_fro(arr, mode, which, f))
-    out["block_fro_max_rel"] = max(fro)
+        r_, a_ = PT.compare_fro(arr, mode, which, f)
+        rel.append(r_)
+        ab.append(a_)
+    out["block_fro_max_rel"] = max(rel)
+    out["block_fro_max_abs_over_factor"] = max(ab)
     samples = PT.leaf_samples(cfg.name)
     if samples is not None:
         stores = {"L": L.store, "U": U.store}
-        worst, nblk = PT.compare_leaf_samples(samples, mode,
-                                              lambda w, u: stores[w].download_leaf(u))
+        totals = {w: PT.factor_norm(arr, mode, w) for w in ("L", "U")}
+        worst, nblk = PT.compare_leaf_samples(samples, mode, lambda w, u: stores[w].download_leaf(u),
+                                              totals)
         out["leaf_entries_max_rel"] = worst
         out["leaf_blocks_compared"] = nblk
     tol = 10 * cfg.eps
-    out["tolerance"] = f"ranks equal; per-block relative Frobenius and entry differences <= 10*eps = {tol:g}"
+    out["tolerance"] = (f"ranks equal; per-block Frobenius difference relative to the block (blocks with "
+                        f">= {PT.SIGNIFICANT:g} of the factor norm) and to the factor norm (all blocks), "
+                        f"sampled leaf entries relative to max(block, {PT.SIGNIFICANT:g} x factor): "
+                        f"all <= 10*eps = {tol:g}")
     ok = (out["rank_mismatches"] == 0 and out["block_fro_max_rel"] <= tol
+          and out["block_fro_max_abs_over_factor"] <= tol
           and out.get("leaf_entries_max_rel", 0.0) <= tol)
     out["ok"] = bool(ok)
     return out, ok

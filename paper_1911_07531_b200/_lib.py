@@ -175,16 +175,24 @@ class Plan:
 
     def __init__(self, ops, task_ops, succ_ptr, succ_idx, wave_ptr, wave_tasks,
                  scratch_doubles, scratch_ranks, max_ctas=0, ctas_per_sm=1, task_scratch=None,
-                 n_big=0):
+                 n_big=0, scratch_budget=None):
         """task_scratch (per-task need, doubles) enables tiered scratch: each
         CTA gets an arena at the 99.9th percentile of the needs; tasks above
-        it share peak-size arenas, one per 4 CTAs (n_big=0) or n_big."""
+        it share peak-size arenas, one per 4 CTAs (n_big=0) or n_big.
+        scratch_budget (bytes, large problems): the per-CTA arenas of all
+        CTAs take at most half of it and the peak-size arenas the other
+        half (at least one)."""
         L = lib()
         big, ts = 0, None
         if task_scratch is not None and len(task_scratch):
             ts = np.ascontiguousarray(task_scratch, dtype=np.int64)
             peak = int(ts.max())
             small = max(int(np.percentile(ts, 99.9)), 1 << 16)
+            if scratch_budget:
+                nct = (max_ctas or 148 * max(1, int(ctas_per_sm)))
+                small = min(small, max(1 << 16, int(scratch_budget) // 2 // 8 // nct))
+                if peak > small:
+                    n_big = max(1, int(scratch_budget) // 2 // 8 // peak)
             if peak > small:
                 scratch_doubles = small
                 big = peak

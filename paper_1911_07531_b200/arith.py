@@ -54,13 +54,18 @@ _PLANS = _PlanCache(PLAN_CACHE_SIZE)
 
 
 def get_plan(table, mode, policy, rank_cap, dag_mode=None, sparsify=False, max_ctas=0,
-             split_min=engine.DEFAULT_SPLIT_MIN, nrep=1, ctas_per_sm=None):
-    """Cached execution plan (planning and upload happen once per tree)."""
+             split_min=engine.DEFAULT_SPLIT_MIN, nrep=1, ctas_per_sm=None, caps=None, acc_budget=0,
+             scratch_budget=None):
+    """Cached execution plan (planning and upload happen once per tree).
+    caps / acc_budget / scratch_budget: rank-bounded arenas, accumulator
+    storage reuse and scratch bounds of large problems (engine.ExecPlan)."""
+    ck = None if caps is None else hash(np.ascontiguousarray(caps, dtype=np.int32).tobytes())
     key = (table, mode, repr(policy), rank_cap, dag_mode, sparsify, max_ctas, split_min, nrep,
-           ctas_per_sm)
+           ctas_per_sm, ck, acc_budget, scratch_budget)
     return _PLANS.get(key, lambda: engine.ExecPlan(
         table, mode, policy, rank_cap, dag_mode=dag_mode, sparsify=sparsify, max_ctas=max_ctas,
-        split_min=split_min, nrep=nrep, ctas_per_sm=ctas_per_sm))
+        split_min=split_min, nrep=nrep, ctas_per_sm=ctas_per_sm, caps=caps, acc_budget=acc_budget,
+        scratch_budget=scratch_budget))
 
 
 def clear_plans():
@@ -84,13 +89,19 @@ def _check_operands(*ms):
 
 
 def run_hlu(A, L, U, policy, mode, exec_mode=engine.EXEC_PERSISTENT, dag_mode=None,
-            sparsify=False, stream=None, split_min=engine.DEFAULT_SPLIT_MIN):
+            sparsify=False, stream=None, split_min=engine.DEFAULT_SPLIT_MIN, acc_budget=0,
+            scratch_budget=None):
     t = _check_operands(A, L, U)
     rc = A.store.layout.rank_cap
+    caps = getattr(A.store.layout, "caps", None)
     for M in (L, U):
         if M.store.layout.rank_cap != rc:
             raise ValueError("L/U storage rank_cap differs from A's")
-    plan = get_plan(t, mode, policy, rc, dag_mode, sparsify, split_min=split_min)
+        mc = getattr(M.store.layout, "caps", None)
+        if (mc is None) != (caps is None) or (caps is not None and not np.array_equal(mc, caps)):
+            raise ValueError("L/U storage capacities differ from A's")
+    plan = get_plan(t, mode, policy, rc, dag_mode, sparsify, split_min=split_min, caps=caps,
+                    acc_budget=acc_budget, scratch_budget=scratch_budget)
     plan.run(A.store, L.store, U.store, exec_mode, stream)
     c = plan.counters(stream)
     counters.add(c["truncations"], c["updates"])

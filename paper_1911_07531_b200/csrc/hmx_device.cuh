@@ -230,6 +230,109 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
   __syncthreads();
 }
 
+// FP64 tensor-core (DMMA, mma.sync m8n8k4) variant of the 64x64 tile path,
+// for the ncu A/B against the DFMA register tiles (HMX_DMMA=1 builds use
+// it for every cta_gemm).  Same k-chunk staging and double buffering as
+// gemm_tiles<4,4,GK>; warp w owns rows 16*(w%4)..+16 and columns
+// 32*(w/4)..+32 of the tile as 2x4 mma tiles of 8x8; per 4-wide k step a
+// thread holds one A and one B element per mma row / column tile
+// (fragment layout of mma.m8n8k4.f64: A[g][t], B[t][g], C[g][2t+i] with
+// g = lane/4, t = lane%4).  The k-order inside one mma is the hardware's,
+// so results differ from the DFMA chains in the last bits.
+#ifndef HMX_DMMA
+#define HMX_DMMA 0
+#endif
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__device__ __noinline__ void gemm_tiles_dmma(int m, int n, int k, double alpha, const double* __restrict__ A,
+                                             int lda, bool ta, const double* __restrict__ B, int ldb,
+                                             bool tb, bool beta1, double* C, int ldc, double* sm) {
+  static_assert(HMX_THREADS == 256, "DMMA tiles assume 8 warps");
+  constexpr int TM = 64, TN = 64, KC = GK, PA = TM + 1, PB = TN + 1;
+  constexpr int SA = KC * PA, SB = KC * PB;
+  constexpr int NL = (TM * KC) / HMX_THREADS;  // 4 loads of A and of B per thread and chunk
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wr = (w & 3) * 16, wc = (w >> 2) * 32;
+  const int tiles_m = (m + TM - 1) / TM, tiles_n = (n + TN - 1) / TN;
+  for (int tile = 0; tile < tiles_m * tiles_n; ++tile) {
+    const int m0 = (tile % tiles_m) * TM, n0 = (tile / tiles_m) * TN;
+    double acc[2][4][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double ra[NL], rb[NL];
+    auto load = [&](int k0) {
+#pragma unroll
+      for (int q = 0; q < NL; ++q) {
+        const int e = tid + q * HMX_THREADS;
+        int i, kk;
+        if (!ta) { i = e % TM; kk = e / TM; } else { kk = e % KC; i = e / KC; }
+        const int gi = m0 + i, gk = k0 + kk;
+        ra[q] = (gi < m && gk < k) ? (ta ? A[gk + (int64_t)gi * lda] : A[gi + (int64_t)gk * lda]) : 0.0;
+        int j, kb;
+        if (!tb) { kb = e % KC; j = e / KC; } else { j = e % TN; kb = e / TN; }
+        const int gj = n0 + j, gkb = k0 + kb;
+        rb[q] = (gj < n && gkb < k) ? (tb ? B[gj + (int64_t)gkb * ldb] : B[gkb + (int64_t)gj * ldb]) : 0.0;
+      }
+    };
+    auto store = [&](int buf) {
+      double* As = sm + buf * (SA + SB);
+      double* Bs = As + SA;
+#pragma unroll
+      for (int q = 0; q < NL; ++q) {
+        const int e = tid + q * HMX_THREADS;
+        int i, kk;
+        if (!ta) { i = e % TM; kk = e / TM; } else { kk = e % KC; i = e / KC; }
+        As[kk * PA + i] = ra[q];
+        int j, kb;
+        if (!tb) { kb = e % KC; j = e / KC; } else { j = e % TN; kb = e / TN; }
+        Bs[kb * PB + j] = rb[q];
+      }
+    };
+    const int nk = (k + KC - 1) / KC;
+    load(0);
+    store(0);
+    __syncthreads();
+    for (int c = 0; c < nk; ++c) {
+      if (c + 1 < nk) load((c + 1) * KC);
+      const double* As = sm + (c & 1) * (SA + SB);
+      const double* Bs = As + SA;
+#pragma unroll
+      for (int k4 = 0; k4 < KC; k4 += 4) {
+        double a[2], b[4];
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri) a[ri] = As[(k4 + tq) * PA + wr + ri * 8 + g];
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) b[ci] = Bs[(k4 + tq) * PB + wc + ci * 8 + g];
+#pragma unroll
+        for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) dmma884(acc[ri][ci][0], acc[ri][ci][1], a[ri], b[ci]);
+      }
+      if (c + 1 < nk) store((c + 1) & 1);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+      for (int ci = 0; ci < 4; ++ci)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int gi = m0 + wr + ri * 8 + g, gj = n0 + wc + ci * 8 + 2 * tq + x;
+          if (gi < m && gj < n) {
+            double* cp = C + gi + (int64_t)gj * ldc;
+            *cp = beta1 ? fma(alpha, acc[ri][ci][x], *cp) : alpha * acc[ri][ci][x];
+          }
+        }
+  }
+  __syncthreads();
+}
+
 // Split-k GEMM for at most 32 output blocks of 4x4 (lane = block) and a
 // long reduction: warp w sums k in [w*k/8, (w+1)*k/8) for every block, the
 // eight partial tiles meet in shared memory (8 x 32 x 16 doubles).
@@ -374,7 +477,11 @@ __device__ __forceinline__ void cta_gemm(int m, int n, int k, double alpha, cons
                                          int lda, bool ta, const double* __restrict__ B, int ldb, bool tb,
                                          bool beta1, double* C, int ldc, double* sm) {
   if (m <= 0 || n <= 0) return;
+#if HMX_DMMA
+  gemm_tiles_dmma(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+#else
   gemm_tiles<4, 4, GK>(m, n, k, alpha, A, lda, ta, B, ldb, tb, beta1, C, ldc, sm);
+#endif
 }
 
 // Shape-adaptive GEMM for the large-block paths (blocked QR / Q

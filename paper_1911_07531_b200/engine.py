@@ -211,7 +211,8 @@ class ExecPlan:
 
     def __init__(self, table: BlockTable, mode: str, policy, rank_cap=None, dag_mode=None,
                  sparsify=False, max_ctas=0, nrep=1, split_min=DEFAULT_SPLIT_MIN,
-                 ctas_per_sm=None, caps=None, python_planner=False, acc_budget=0, big_budget=None):
+                 ctas_per_sm=None, caps=None, python_planner=False, acc_budget=0,
+                 scratch_budget=None):
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
         self.table = table
@@ -281,7 +282,7 @@ class ExecPlan:
         tsc = prog.task_scratch if self.nrep == 1 else np.tile(prog.task_scratch, self.nrep)
         self.plan = _lib.Plan(ops, task_ops, ptr, idx, self.wave_ptr, self.wave_tasks,
                               prog.scratch_doubles, prog.scratch_ranks, max_ctas, self.ctas_per_sm,
-                              task_scratch=tsc)
+                              task_scratch=tsc, scratch_budget=scratch_budget)
         torch = _torch()
         self.acc_values = torch.zeros(prog.acc_size * self.nrep, dtype=torch.float64, device="cuda")
         self.acc_ranks = torch.zeros(max(table.n, 1) * self.nrep, dtype=torch.int32, device="cuda")

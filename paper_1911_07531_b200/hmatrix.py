@@ -595,3 +595,15 @@ def leaf_update(C: HMatrix, alpha: float, A: HMatrix, B: HMatrix, policy: Trunca
     p.run(A.store, B.store, C.store)
     c = p.counters()
     counters.add(c["truncations"], c["updates"])
+
+
+def __getattr__(name):
+    """Payload helpers of the reference's hmatrix module (hmatrix.py:349-448)
+    live in payload.py (device arithmetic); resolved lazily to avoid an
+    import cycle."""
+    if name in ("product_payload", "fold_payload_into_leaf", "scatter_payload", "payload_dense",
+                "payload_shape", "payload_restrict"):
+        from . import payload
+
+        return getattr(payload, name)
+    raise AttributeError(name)

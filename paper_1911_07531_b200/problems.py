@@ -108,3 +108,26 @@ def one_d_problem(n: int):
     x = (np.arange(n) + 0.5) / n
     diag = (np.log(1.0 / (2.0 * n)) - 1.0) / n
     return Geometry(x[:, None]), PointKernel(x[:, None], np.log, diag_value=diag, scale=1.0 / n)
+
+
+def fibonacci_sphere(n: int) -> np.ndarray:
+    """n quasi-uniform points on the unit sphere: golden-angle spiral in z
+    (problems.py:95-102)."""
+    i = np.arange(n, dtype=float)
+    z = 1.0 - 2.0 * (i + 0.5) / n
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = np.pi * (3.0 - np.sqrt(5.0)) * i
+    return np.column_stack([r * np.cos(phi), r * np.sin(phi), z])
+
+
+def sphere_problem(n: int):
+    """1/r kernel on the unit sphere with quadrature weight w = 4 pi / n and
+    the flat-disc self term 2 sqrt(pi w) on the diagonal (problems.py:105-119)."""
+    from .trees import Geometry
+
+    if n < 4:
+        raise ValueError("sphere problem needs n >= 4")
+    pts = fibonacci_sphere(n)
+    w = 4.0 * np.pi / n
+    return Geometry(pts), PointKernel(pts, lambda d: 1.0 / d, diag_value=2.0 * np.sqrt(np.pi * w),
+                                      scale=w)

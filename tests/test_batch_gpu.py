@@ -64,3 +64,40 @@ def test_hbatch_replicas_equal_single(mode):
             d1 = X1.to_dense()
             d = X.member(b).to_dense()
             assert np.linalg.norm(d - d1) <= 1e-9 * np.linalg.norm(d1)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_batched_variant_matches_reference(name):
+    """The 2-CTAs-per-SM executor (k_persistent<2>, 110 KB shared memory),
+    used for replica throughput, reproduces the reference's run on a
+    BASELINE config: every L/U rank of every member equal to the fixture,
+    per-block factor norms within 10*eps (tests/parity.py)."""
+    if not have(name):
+        pytest.skip("fixture missing")
+    from paper_1911_07531_b200 import configs, hmatrix as H
+    from paper_1911_07531_b200.arith import hlu_batch
+    from tests import parity as PT
+
+    meta, arr = load(name)
+    cfg = configs.config(name)
+    geom, root, perm, broot = configs.structure(cfg)
+    pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
+    A = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+    R = 2
+    AB = H.HBatch.replicate(A, R)
+    LB, UB = H.HBatch(broot, pol, R, 64), H.HBatch(broot, pol, R, 64)
+    plan = hlu_batch(AB, LB, UB, pol, "accu", ctas_per_sm=2)
+    assert plan.ctas_per_sm == 2
+    tot = {w: PT.factor_norm(arr, "accu", w) for w in ("L", "U")}
+    for b in range(R):
+        Lm, Um = LB.member(b), UB.member(b)
+        assert PT.compare_ranks(arr, "accu", Lm.store.ranks.cpu().numpy(), Um.store.ranks.cpu().numpy()) == 0
+        for which, M in (("L", Lm), ("U", Um)):
+            f = PT.store_fro(M.store.layout, M.store.values.cpu().numpy(), M.store.ranks.cpu().numpy())
+            rel, ab = PT.compare_fro(arr, "accu", which, f)
+            assert rel <= 10 * cfg.eps and ab <= 10 * cfg.eps, (which, rel, ab)
+        samples = PT.leaf_samples(name)
+        if samples is not None:
+            stores = {"L": Lm.store, "U": Um.store}
+            worst, nblk = PT.compare_leaf_samples(samples, "accu", lambda w, u: stores[w].download_leaf(u), tot)
+            assert nblk > 0 and worst <= 10 * cfg.eps, worst

@@ -100,7 +100,7 @@ def test_sparsified_dag_execution_bitwise_identical(mode):
     A, pol, eps = oracle_A("s2")
     a = run_device("s2", mode, A.lv, split_min=32)
     b = run_device("s2", mode, A.lv, split_min=32, sparsify=True)
-    assert b[3].dag.n_edges < a[3].dag.n_edges
+    assert b[3].n_dag_edges < a[3].n_dag_edges
     assert b[3].n_dag_edges <= a[3].n_dag_edges
     for x, y in zip(a[:2], b[:2]):
         for u, v in x.items():
@@ -192,6 +192,20 @@ def test_config_ranks_bit_exact_vs_reference(name, mode):
     sel = arr[f"{mode}_L_rank"] >= 0
     assert np.array_equal(rl[sel], arr[f"{mode}_L_rank"][sel]), int((rl[sel] != arr[f"{mode}_L_rank"][sel]).sum())
     assert np.array_equal(ru[sel], arr[f"{mode}_U_rank"][sel]), int((ru[sel] != arr[f"{mode}_U_rank"][sel]).sum())
+    # per-block factors: Frobenius norms of every block and the entries of
+    # sampled leaves vs the reference's run (tests/parity.py, 10*eps)
+    from tests import parity as PT
+
+    tot = {w: PT.factor_norm(arr, mode, w) for w in ("L", "U")}
+    for which, M in (("L", L), ("U", U)):
+        f = PT.store_fro(M.store.layout, M.store.values.cpu().numpy(), M.store.ranks.cpu().numpy())
+        rel, ab = PT.compare_fro(arr, mode, which, f)
+        assert rel <= 10 * cfg.eps and ab <= 10 * cfg.eps, (which, rel, ab)
+    samples = PT.leaf_samples(name)
+    if samples is not None and f"{mode}_L_meta" in samples:
+        stores = {"L": L.store, "U": U.store}
+        worst, nblk = PT.compare_leaf_samples(samples, mode, lambda w, u: stores[w].download_leaf(u), tot)
+        assert nblk > 0 and worst <= 10 * cfg.eps, worst
     # probe through the oracle's apply on the downloaded factors
     Lh, Uh = O.HM(bt, L.store.download_leaves()), O.HM(bt, U.store.download_leaves())
     got = O.apply(Lh, 0, O.apply(Uh, 0, X))
