@@ -468,11 +468,11 @@ class DensePlan:
     triangular solves (one sequential task).  Bases: 0 = the H-matrix pool,
     1 = X / Y (column-major, device), 2 = the output of apply / apply_t."""
 
-    def __init__(self, table: BlockTable, op: str, uid: int, cols: int, rank_cap=None):
+    def __init__(self, table: BlockTable, op: str, uid: int, cols: int, rank_cap=None, layout=None):
         from .planner import plan_dense
 
         self.table, self.op, self.uid, self.cols = table, op, int(uid), int(cols)
-        prog = plan_dense(table, op, uid, cols, rank_cap)
+        prog = plan_dense(table, op, uid, cols, rank_cap, layout)
         self.prog = prog
         self.layout = prog.layout
         n = len(prog.keys)
@@ -485,6 +485,11 @@ class DensePlan:
     def run(self, H: HStore, X, out=None, stream=None):
         if H.layout.table is not self.table:
             raise ValueError("operand is not over the plan's block tree")
+        if H.layout is not self.layout and not (
+                np.array_equal(H.layout.u_off, self.layout.u_off)
+                and np.array_equal(H.layout.d_off, self.layout.d_off)
+                and np.array_equal(H.layout.cap, self.layout.cap)):
+            raise ValueError("operand storage layout differs from the plan's")
         self.plan.bind(0, H.values, H.ranks)
         self.plan.bind(1, X, None)
         if out is not None:

@@ -470,8 +470,9 @@ def _dense_plan(M: HMatrix, op, cols):
     if _DENSE_PLANS is None:
         _DENSE_PLANS = _PlanCache(16)
     t = M.table
-    key = (t, op, M.uid, int(cols), M.store.layout.rank_cap)
-    return _DENSE_PLANS.get(key, lambda: DensePlan(t, op, M.uid, cols, M.store.layout.rank_cap))
+    lay = M.store.layout
+    key = (t, op, M.uid, int(cols), lay.rank_cap, int(lay.size), id(lay.caps) if lay.caps is not None else 0)
+    return _DENSE_PLANS.get(key, lambda: DensePlan(t, op, M.uid, cols, lay.rank_cap, lay))
 
 
 def _dense_run(M: HMatrix, op, X, out_rows):

@@ -1143,7 +1143,7 @@ def _elementary(bounds_lo, bounds_hi, lo, hi):
     return list(zip(cuts[:-1], cuts[1:]))
 
 
-def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
+def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None, layout=None):
     """Program of an H x dense operation on block u (hmatrix.py:286-341).
 
     apply:         out = H[u] @ X            H=0, X=1 (n_u x cols), out=2 (m_u x cols)
@@ -1163,7 +1163,9 @@ def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
         raise ValueError(op)
     from .hmatrix import EXACT
 
-    lay = Layout(table, rank_cap)
+    # the operand's own layout when given (rank-bounded arenas of
+    # assemble_bounded / zeros(..., caps) differ from the rank_cap layout)
+    lay = layout if layout is not None else Layout(table, rank_cap)
     H = PMat(0, lay)
     p = Planner(EXACT, rank_cap, 0)
     t = table
@@ -1180,15 +1182,23 @@ def plan_dense(table: BlockTable, op: str, u: int, cols: int, rank_cap=None):
             ivs = _elementary([t.r0[v] for v in leaves], [t.r1[v] for v in leaves], lo0, hi0)
         X = Ref(1, 0, max(n_u if not tr else m_u, 1))
         O = Ref(2, 0, max(m_u if not tr else n_u, 1))
-        for a, b in ivs:
+        # leaves crossing each elementary interval, in block pre-order (one
+        # pass over the leaves: linear in the number of crossings)
+        starts = np.asarray([a for a, _ in ivs], dtype=np.int64)
+        crossing = [[] for _ in ivs]
+        for v in leaves:
+            vlo, vhi = (int(t.c0[v]), int(t.c1[v])) if tr else (int(t.r0[v]), int(t.r1[v]))
+            i0 = int(np.searchsorted(starts, vlo, side="left"))
+            i1 = int(np.searchsorted(starts, vhi, side="left"))
+            for i in range(i0, i1):
+                crossing[i].append(v)
+        for (a, b), vs in zip(ivs, crossing):
             p.begin("dense_" + op, (op, u, a))
             rows = b - a
             out = O.at(a - lo0)
             p.zero(rows, cols, out)
-            for v in leaves:
+            for v in vs:
                 vlo, vhi = (int(t.c0[v]), int(t.c1[v])) if tr else (int(t.r0[v]), int(t.r1[v]))
-                if vhi <= a or vlo >= b:
-                    continue
                 off = a - vlo  # slice of the leaf's rows (apply) / columns (apply_t)
                 if not tr:
                     c0, nv = int(t.c0[v] - t.c0[u]), int(t.nc[v])
