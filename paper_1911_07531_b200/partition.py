@@ -25,11 +25,16 @@ Two launch forms share the records: ``rank=-1`` emulates every rank in one
 launch on one GPU (CTA c serves rank c mod nranks; each rank's storage is a
 replica in the same pools, the ops and records carry the replica offsets),
 used by the tests to prove the protocol bit-exact; ``rank>=0`` (one
-process per GPU, peers' storage mapped through CUDA IPC with
-hmx_plan_peer) is rejected by :class:`PartitionedPlan` until a
-multi-process runner exists: the launch needs every rank reset, a
-cross-rank barrier, then a no-reset launch (mode 4), and it cannot be
-exercised on the single-GPU test boxes of this build.
+process per GPU) is driven by :class:`DistributedHLU`: every rank builds the
+same partition, exports CUDA IPC handles of its pools and scheduler state
+over ``torch.distributed``, maps its peers' (hmx_plan_peer), then per run
+resets its scheduler, meets the others at a barrier and launches without
+reset (mode 4).  Ranks wait on one another inside the launch, so each rank
+needs its own GPU (two such kernels time-sliced on one GPU stall each
+other until the driver's context-switch watchdog fires): on the
+single-GPU boxes of this build only the emulated form runs on the device;
+the host protocol of DistributedHLU is covered by the gloo world-2 test
+(tests/test_partition_cpu.py) with the device calls recorded.
 """
 
 from __future__ import annotations
@@ -287,15 +292,15 @@ class PartitionedPlan:
     """
 
     def __init__(self, table, mode, policy, rank_cap, nranks, rank=-1, split_min=None,
-                 ctas_per_sm=1, max_ctas=0):
+                 ctas_per_sm=1, max_ctas=0, _multiprocess=False):
         from . import engine
 
         if mode not in ("std", "accu"):
             raise ValueError("mode must be 'std' or 'accu'")
-        if int(rank) >= 0:
+        if int(rank) >= 0 and not _multiprocess:
             raise NotImplementedError(
-                "multi-process partitioned H-LU (rank >= 0) is not supported: only the "
-                "emulated launch (rank=-1) is implemented and tested")
+                "a real rank (rank >= 0) needs its peers mapped before the launch: "
+                "use DistributedHLU (one process per GPU)")
         split_min = engine.DEFAULT_SPLIT_MIN if split_min is None else split_min
         self.table, self.mode, self.policy, self.rank_cap = table, mode, policy, rank_cap
         self.nranks, self.rank = int(nranks), int(rank)
@@ -392,4 +397,173 @@ class PartitionedPlan:
         return out
 
 
-__all__ = ["Partition", "PartitionedPlan", "row_bounds", "simulate", "PUB_DTYPE"]
+# ----------------------------------------------------------------------
+# one process per GPU
+# ----------------------------------------------------------------------
+class _Backend:
+    """Device calls of DistributedHLU (replaced by a recorder in the CPU test)."""
+
+    ipc_handle = staticmethod(lambda ptr: _lib.ipc_handle(ptr))
+    ipc_open = staticmethod(lambda handle: _lib.ipc_open(handle))
+    ipc_close = staticmethod(lambda base: _lib.ipc_close(base))
+
+    @staticmethod
+    def synchronize():
+        _torch().cuda.synchronize()
+
+
+def export_table(pointers, backend=_Backend):
+    """{name: address} -> {name: (ipc handle bytes, offset)} (0 stays None)."""
+    out = {}
+    for k, ptr in pointers.items():
+        out[k] = None if not ptr else tuple(backend.ipc_handle(int(ptr)))
+    return out
+
+
+def import_table(table, opened, backend=_Backend):
+    """Peer's exported table -> {name: address in this process}.  Several
+    pools may live in one allocation (torch's caching allocator): every
+    handle is opened once (``opened``: handle bytes -> mapped base)."""
+    out = {}
+    for k, v in table.items():
+        if v is None:
+            out[k] = 0
+            continue
+        handle, off = v
+        base = opened.get(handle)
+        if base is None:
+            base = opened[handle] = int(backend.ipc_open(handle))
+        out[k] = base + int(off)
+    return out
+
+
+class DistributedHLU:
+    """Block-row partitioned H-LU, one process per GPU.
+
+    ``torch.distributed`` must be initialised (NCCL on the GPUs; the object
+    collectives used here also run on gloo).  Every rank holds full-size
+    pools; it executes the tasks of its block rows and receives the objects
+    it reads from the ranks that produce them (hmx_pub records, written by
+    the producer's CTA straight into this rank's pools over NVLink).
+
+        d = DistributedHLU(table, "accu", policy, rank_cap)
+        A, L, U = d.stores(A_full)        # this rank's pools
+        d.connect(A, L, U)                # IPC exchange, once per storage
+        d.run()                           # reset, barrier, launch, status
+        Lfull = d.collect(L, 1)           # all-reduce of the owned leaves
+    """
+
+    BASES = (0, 1, 2, ACC_BASE_ID, WS_BASE_ID)
+
+    def __init__(self, table, mode, policy, rank_cap, group=None, split_min=None, ctas_per_sm=1,
+                 max_ctas=0, backend=_Backend, plan=None):
+        import torch.distributed as dist
+
+        self.dist, self.group, self.backend = dist, group, backend
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        if self.nranks < 2:
+            raise ValueError("DistributedHLU needs at least two ranks")
+        self.pp = plan if plan is not None else PartitionedPlan(
+            table, mode, policy, rank_cap, self.nranks, self.rank, split_min, ctas_per_sm, max_ctas,
+            _multiprocess=True)
+        self.part = self.pp.part
+        self._opened = {}
+        self._connected = False
+
+    def stores(self, A):
+        """This rank's pools: a copy of A and zero L, U."""
+        return self.pp.stores(A)
+
+    def _pointers(self, A, L, U):
+        pp = self.pp
+        t = {}
+        for b, (v, r) in zip(self.BASES, ((A.values, A.ranks), (L.values, L.ranks), (U.values, U.ranks),
+                                          (pp.acc_values, pp.acc_ranks), (pp.ws_values, pp.ws_ranks))):
+            t[f"v{b}"] = v.data_ptr() if v.numel() else 0
+            t[f"r{b}"] = r.data_ptr() if r.numel() else 0
+        t["indeg"], t["queue"], t["qctl"] = pp.plan.sched_state()
+        return t
+
+    def connect(self, A, L, U):
+        """Bind this rank's pools and map every peer's pools and scheduler
+        state (one all_gather of the IPC handle tables)."""
+        self.pp.bind(A, L, U)
+        mine = export_table(self._pointers(A, L, U), self.backend)
+        tables = [None] * self.nranks
+        self.dist.all_gather_object(tables, mine, group=self.group)
+        for r, tab in enumerate(tables):
+            if r == self.rank:
+                continue
+            adr = import_table(tab, self._opened, self.backend)
+            bases, rbases = [0] * 16, [0] * 16
+            for b in self.BASES:
+                bases[b], rbases[b] = adr[f"v{b}"], adr[f"r{b}"]
+            self.pp.plan.peer(r, bases, rbases, adr["indeg"], adr["queue"], adr["qctl"])
+        self._connected = True
+        self.dist.barrier(group=self.group)
+
+    def run(self, stream=None, check=True):
+        """One factorization.  Every rank resets its own scheduler state
+        BEFORE the barrier: a peer may release tasks of this rank as soon as
+        it starts, so no rank may launch while another still resets."""
+        if not self._connected:
+            raise RuntimeError("connect(A, L, U) first")
+        plan = self.pp.plan
+        plan.reset_counters(stream)
+        plan.reset(stream)
+        self.backend.synchronize()
+        self.dist.barrier(group=self.group)
+        plan.execute(4, stream)
+        if check:
+            self.pp.check(stream)
+        self.dist.barrier(group=self.group)
+
+    def owned_leaves(self, base_id):
+        """Leaves of matrix ``base_id`` whose final version this rank wrote."""
+        t, part = self.pp.table, self.part
+        out = []
+        for u in t.leaves(0):
+            w = part.final_writer.get(("m", base_id, u))
+            if (int(part.owner[w]) if w is not None else 0) == self.rank:
+                out.append(int(u))
+        return out
+
+    def collect(self, S, base_id):
+        """Full matrix ``base_id`` on every rank: each rank contributes the
+        leaves it wrote last, one all-reduce (outside the factorization)."""
+        from .engine import HStore
+
+        torch = _torch()
+        lay, t = self.pp.layout, self.pp.table
+        out = HStore(lay)
+        out.values.zero_()
+        out.ranks.zero_()
+        idx, ridx = [], []
+        for u in self.owned_leaves(base_id):
+            if t.adm[u]:
+                a, b = int(lay.u_off[u]), int(lay.v_off[u] + t.nc[u] * lay.cap[u])
+            else:
+                a, b = int(lay.d_off[u]), int(lay.d_off[u] + t.m[u] * t.nc[u])
+            idx.append(np.arange(a, b))
+            ridx.append(u)
+        if idx:
+            ii = torch.from_numpy(np.concatenate(idx)).to(S.values.device)
+            out.values[ii] = S.values[ii]
+            rr = torch.from_numpy(np.asarray(ridx)).to(S.ranks.device)
+            out.ranks[rr] = S.ranks[rr]
+        self.dist.all_reduce(out.values, group=self.group)
+        self.dist.all_reduce(out.ranks, group=self.group)
+        return out
+
+    def close(self):
+        for base in self._opened.values():
+            try:
+                self.backend.ipc_close(base)
+            except Exception:
+                pass
+        self._opened = {}
+        self._connected = False
+
+
+__all__ = ["Partition", "PartitionedPlan", "DistributedHLU", "row_bounds", "simulate", "PUB_DTYPE",
+           "export_table", "import_table"]

@@ -121,3 +121,155 @@ def test_two_ranks_derive_the_same_partition():
         assert p.exitcode == 0
     assert out[0][0] == out[1][0]
     assert out[0][1] + out[1][1] == nt
+
+
+# ----------------------------------------------------------------------
+# DistributedHLU host protocol (gloo, world 2): the device calls are
+# recorded; what is checked is what every rank hands to hmx_plan_peer and
+# the order reset -> barrier -> launch(4) -> status.
+# ----------------------------------------------------------------------
+class _FakePlan:
+    def __init__(self, rank, log):
+        self.rank, self.log = rank, log
+        self.state = (0x1000 * (rank + 1) + 0x100000, 0x2000 * (rank + 1) + 0x200000,
+                      0x3000 * (rank + 1) + 0x300000)
+
+    def sched_state(self):
+        return self.state
+
+    def peer(self, r, bases, rbases, indeg, queue, qctl):
+        self.log.append(("peer", r, tuple(bases), tuple(rbases), indeg, queue, qctl))
+
+    def bind(self, *a):
+        self.log.append(("bind", a[0]))
+
+    def reset(self, stream=None):
+        self.log.append(("reset",))
+
+    def reset_counters(self, stream=None):
+        self.log.append(("reset_counters",))
+
+    def execute(self, mode, stream=None):
+        self.log.append(("execute", mode))
+
+    def status(self, stream=None):
+        self.log.append(("status",))
+        return 0
+
+
+class _FakeBackend:
+    """An 'IPC handle' names (rank, 4 KiB page); opening it maps the page at
+    (1 << 44) * (rank + 1) + page, so a peer address is recomputable."""
+    rank = 0
+    log = None
+
+    @classmethod
+    def ipc_handle(cls, ptr):
+        page = ptr & ~0xfff
+        return (cls.rank.to_bytes(8, "little") + page.to_bytes(8, "little")).ljust(64, b"\0"), ptr & 0xfff
+
+    @classmethod
+    def ipc_open(cls, handle):
+        r, page = int.from_bytes(handle[:8], "little"), int.from_bytes(handle[8:16], "little")
+        cls.log.append(("open", r, page))
+        return ((1 << 44) * (r + 1)) + page
+
+    @classmethod
+    def ipc_close(cls, base):
+        cls.log.append(("close", base))
+
+    @classmethod
+    def synchronize(cls):
+        cls.log.append(("sync",))
+
+
+def _mapped(r, ptr):
+    return 0 if not ptr else ((1 << 44) * (r + 1)) + ptr
+
+
+def _dworker(rank, world, port, q):
+    import torch
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prog, bt = _prog("s2", "accu")
+    log = []
+    _FakeBackend.rank, _FakeBackend.log = rank, log
+
+    class PP:  # what DistributedHLU uses of a PartitionedPlan
+        part = P.Partition(prog, bt, world)
+        plan = _FakePlan(rank, log)
+        table, layout = bt, prog.layout
+        acc_values = torch.zeros(16, dtype=torch.float64)
+        acc_ranks = torch.zeros(4, dtype=torch.int32)
+        ws_values = torch.zeros(0, dtype=torch.float64)  # empty pool: exported as None
+        ws_ranks = torch.zeros(4, dtype=torch.int32)
+
+        @classmethod
+        def bind(cls, A, L, U):
+            log.append(("bind_stores",))
+
+        @classmethod
+        def check(cls, stream=None):
+            cls.plan.status()
+
+    class S:
+        def __init__(self):
+            self.values = torch.zeros(32, dtype=torch.float64)
+            self.ranks = torch.zeros(8, dtype=torch.int32)
+
+    A, L, U = S(), S(), S()
+    d = P.DistributedHLU(bt, "accu", None, 64, backend=_FakeBackend, plan=PP)
+    d.connect(A, L, U)
+    ptrs = d._pointers(A, L, U)
+    d.run()
+    owned = [len(d.owned_leaves(b)) for b in (1, 2)]
+    d.close()
+    allp = [None] * world
+    dist.all_gather_object(allp, ptrs)
+    if rank == 0:
+        q.put((log, allp, owned, int(bt.leaf.sum())))
+    out = [None] * world
+    dist.all_gather_object(out, owned)
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_distributed_runner_host_protocol_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dworker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    log, allp, owned0, nleaves = q.get(timeout=300)
+    owned = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # rank 0 mapped rank 1's pools and scheduler state, and only those
+    peers = [e for e in log if e[0] == "peer"]
+    assert [e[1] for e in peers] == [1]
+    _, r, bases, rbases, indeg, queue, qctl = peers[0]
+    p1 = allp[1]
+    for b in P.DistributedHLU.BASES:
+        assert bases[b] == _mapped(1, p1[f"v{b}"])
+        assert rbases[b] == _mapped(1, p1[f"r{b}"])
+    assert bases[P.WS_BASE_ID] == 0  # the empty pool travels as a null address
+    assert (indeg, queue, qctl) == tuple(_mapped(1, p1[k]) for k in ("indeg", "queue", "qctl"))
+    # every 4 KiB page is opened once even when several pools share it
+    opens = [e for e in log if e[0] == "open"]
+    assert len(opens) == len(set(opens))
+    # run(): the scheduler is reset and the device idle before the barrier, the launch
+    # does not reset again (mode 4), the status is read after it
+    names = [e[0] for e in log]
+    i_reset, i_sync, i_exec, i_stat = (names.index("reset"), names.index("sync"),
+                                        names.index("execute"), names.index("status"))
+    assert i_reset < i_sync < i_exec < i_stat
+    assert log[i_exec] == ("execute", 4)
+    # the final versions of the factors' leaves are spread over the ranks without overlap
+    assert owned[0][0] + owned[1][0] == nleaves and owned[0][1] + owned[1][1] == nleaves
+    assert min(owned[0] + owned[1]) > 0
