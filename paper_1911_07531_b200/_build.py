@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmx.so")
 DAG_LIB = os.path.join(HERE, "libhmxdag.so")  # host C++: native DAG builder (hmx_dag.cpp)
 SOURCES = ["hmx_engine.cu", "hmx_transfer.cu"]
-HEADERS = ["hmx_device.cuh", os.path.join("..", "..", "include", "hmx.h")]
+HEADERS = ["hmx_device.cuh", "hmx_ws.cuh", os.path.join("..", "..", "include", "hmx.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

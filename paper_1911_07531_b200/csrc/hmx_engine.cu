@@ -23,6 +23,7 @@
 
 #include "../../include/hmx.h"
 #include "hmx_device.cuh"
+#include "hmx_ws.cuh"
 
 using namespace hmx;
 
@@ -286,6 +287,461 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
   }
 }
 
+#ifndef HMX_WS
+#define HMX_WS 2  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path
+#endif
+
+// Core of both warp-synchronous truncation paths, after G (p x q, shared
+// memory, ld lg) holds Ru Rv^T: rank-revealing QR, Jacobi on R1^T, keep,
+// then Yu (p x r, ld ly) = Q_G [J Sigma; 0] (kept columns) and X (q x k,
+// ld lx) with its kept columns ord[t] scaled to W' = Z_r.  Returns r.
+// Work arrays in shared memory: tpg, wdg, rdg, sig (q doubles each), perm,
+// pos, ord (q ints each), xr (24 doubles), Bu (p x min(p,q), ld ly).
+// Every thread of the CTA calls this; ends synchronised.
+struct WsCore {
+  double *G, *Wc, *X, *Yu, *Bu, *tpg, *wdg, *rdg, *sig, *xr;
+  int *perm, *pos, *ord;
+  int lg, lx, ly, lwc;
+  // striu(W^T W) jobs of the outer factors, done by the warps the
+  // rank-revealing QR leaves idle
+  int nsm;
+  double* sA[2];
+  const double* swd[2];
+  int sld[2], srows[2], sp[2];
+  // late allocation (dense_to_lowrank): Wc, X, Yu, Bu are carved out of
+  // `free2` (cap2 doubles) once the revealed rank k is known; if they do not
+  // fit next to G, G moves to `gev` (global, ld ldev) and its storage joins
+  // the free area; if they still do not fit ws_core returns -1 untouched
+  bool late;
+  double* free2;
+  int64_t cap2;
+  double* gev;
+  int ldev;
+};
+
+__device__ __noinline__ int ws_core(const DevPlan& P, const hmx_op& o, int p, int q, WsCore& w,
+                                    double* sm, unsigned long long& tq, int* k_out) {
+  int* ired = reinterpret_cast<int*>(sm + 16);
+  int* flag = reinterpret_cast<int*>(sm + 24);
+  const int tid = threadIdx.x;
+  const int policy = o.iarg[0];
+  const double cut = (policy == 2) ? o.farg[1] : 1e-14;
+  const double thr = HMX_RRQR_THR * cut;
+  const int nwr = (q + 31) >> 5;  // q <= 128 here
+  if ((tid >> 5) < nwr) {
+    const int k = ws_rrqr(p, q, w.G, w.lg, w.tpg, w.wdg, w.rdg, w.perm, w.pos, thr, w.xr, 0, nwr, 3);
+    if (tid == 0) ired[0] = k;
+  } else {
+    for (int x = 0; x < w.nsm; ++x)
+      ws_smat(w.srows[x], w.sp[x], w.sA[x], w.sld[x], w.swd[x], tid - nwr * 32, HMX_THREADS - nwr * 32);
+  }
+  __syncthreads();
+  const int k = ired[0];
+  *k_out = k;
+  phase(P, 13, tq);
+  if (w.late) {
+    const int64_t need = (int64_t)(w.lg + w.lx + 2 * w.ly) * max(k, 1);
+    double* base = w.free2;
+    if (need > w.cap2) {
+      if (!w.gev || need > w.cap2 + (w.free2 - w.G)) return -1;
+      FOR_MN(i, c, p, q) w.gev[i + (int64_t)c * w.ldev] = w.G[i + c * w.lg];
+      __syncthreads();
+      base = w.G;
+      w.G = w.gev;
+      w.lg = w.ldev;
+    }
+    const int lw = p | 1;
+    w.Wc = base;
+    w.X = w.Wc + (int64_t)lw * max(k, 1);
+    w.Yu = w.X + (int64_t)w.lx * max(k, 1);
+    w.Bu = w.Yu + (int64_t)w.ly * max(k, 1);
+    w.lwc = lw;
+  }
+  // X = R1^T (q x k); Wc = the reflector tails in pivot order (p x k)
+  FOR_MN(c, i, q, k) {
+    const int pc = w.pos[c];
+    w.X[c + i * w.lx] = pc > i ? w.G[i + (int64_t)c * w.lg] : (pc == i ? w.rdg[i] : 0.0);
+  }
+  FOR_MN(i, j, p, k) w.Wc[i + j * w.lwc] = (i > j) ? w.G[i + (int64_t)w.perm[j] * w.lg] : 0.0;
+  __syncthreads();
+  int sweeps = 0;
+  if (k > 0 && !ws_jacobi(q, k, w.X, w.lx, w.sig, w.ord, flag, &sweeps))
+    if (tid == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
+  phase(P, 14, tq, sweeps);
+  int r = keep_count(policy, o.iarg[1], o.farg[1], w.sig, w.ord, k);
+  const int cap = o.iarg[2];
+  if (r > cap) {
+    if (tid == 0) set_status(P, HMX_ERR_RANK_OVERFLOW);
+    r = cap;
+  }
+  if (r == 0) return 0;
+  // Yu[i, t] = (R1 X[:, ord t])_i / sigma_t  (= (J Sigma)[i, t]), rows k..p-1 zero
+  for (int e = tid; e < p * r; e += HMX_THREADS) {
+    const int i = e % p, t = e / p;
+    double s0 = 0.0, s1 = 0.0;
+    if (i < k) {
+      const double* x = w.X + (int64_t)w.ord[t] * w.lx;
+      const double rdi = w.rdg[i];
+      for (int c = 0; c < q; c += 4) {
+        double g[4], xv[4];
+        int pc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = min(c + u, q - 1);
+          pc[u] = w.pos[cc];
+          g[u] = w.G[i + (int64_t)cc * w.lg];
+          xv[u] = (c + u < q) ? x[cc] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u += 2) {
+          s0 = fma(pc[u] > i ? g[u] : (pc[u] == i ? rdi : 0.0), xv[u], s0);
+          s1 = fma(pc[u + 1] > i ? g[u + 1] : (pc[u + 1] == i ? rdi : 0.0), xv[u + 1], s1);
+        }
+      }
+      s0 = (s0 + s1) / w.sig[w.ord[t]];
+    }
+    w.Yu[i + t * w.ly] = s0;
+  }
+  ws_smat(p, k, w.Wc, w.lwc, w.wdg, tid, HMX_THREADS);
+  __syncthreads();
+  // kept columns of X become W' = X / sigma;  Yu := Q_G Yu
+  for (int e = tid; e < q * r; e += HMX_THREADS) {
+    const int c = e % q, col = w.ord[e / q];
+    w.X[c + (int64_t)col * w.lx] /= w.sig[col];
+  }
+  ws_wtb(k, k, w.Wc, w.lwc, w.wdg, w.Yu, w.ly, nullptr, r, w.Bu, w.ly, tid, HMX_THREADS);
+  __syncthreads();
+  ws_trsolve(k, w.Wc, w.lwc, w.tpg, w.Bu, w.ly, r, tid, HMX_THREADS);
+  __syncthreads();
+  ws_wz(p, k, w.Wc, w.lwc, w.wdg, w.Yu, w.ly, nullptr, p, w.Bu, w.ly, r, w.Yu, w.ly, tid, HMX_THREADS);
+  __syncthreads();
+  return r;
+}
+
+// Truncation with U, V, G and all work arrays in shared memory (K <= 64).
+// Returns false (nothing touched) when the shapes do not fit.
+__device__ __noinline__ bool trunc_ws_small(const DevPlan& P, const hmx_op& o, int m, int n, int K, const double* U,
+                               int ldu, const double* V, int ldv, double* Uo, int lduo, double* Vo,
+                               int ldvo, int* rslot, double* sm, unsigned long long& tq) {
+  const int p = min(m, K), q = min(n, K), s = min(p, q);
+  if (K > 64) return false;
+  const int nwg = HMX_WARPS / 2;
+  const int ct = K <= 32 ? 1 : 2;
+  const int mp = ws_qr_rows(m, nwg, ct), np_ = ws_qr_rows(n, nwg, ct);  // zero-padded row counts
+  const int lus = mp | 1, lvs = np_ | 1, lg = p | 1, lx = q | 1, ly = p | 1;
+  const int64_t need = (int64_t)(lus + lvs) * K + (int64_t)lg * q + (int64_t)lg * s + (int64_t)lx * s +
+                       2 * (int64_t)ly * s + (int64_t)lx * s + 12 * K + 4 * (nwg + 1) * (K + 1) + 64;
+  if (need > P.smem_work) return false;
+  double* wp = sm + 32;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
+  double* Us = take((int64_t)lus * K);
+  double* Vs = take((int64_t)lvs * K);
+  WsCore w;
+  w.lg = lg; w.lx = lx; w.ly = ly; w.lwc = lg; w.late = false;
+  w.G = take((int64_t)lg * q);
+  w.Wc = take((int64_t)lg * s);
+  w.X = take((int64_t)lx * s);
+  w.Yu = take((int64_t)ly * s);
+  w.Bu = take((int64_t)ly * s);
+  double* Bv = take((int64_t)lx * s);
+  double* tpu = take(K); double* wdu = take(K);
+  double* tpv = take(K); double* wdv = take(K);
+  w.tpg = take(K); w.wdg = take(K); w.rdg = take(K); w.sig = take(K);
+  w.perm = reinterpret_cast<int*>(take(K));  // perm, pos
+  w.pos = w.perm + K;
+  w.ord = reinterpret_cast<int*>(take(K));
+  w.xr = take(32);
+  double* xchu = take(2 * (nwg + 1) * (K + 1));
+  double* xchv = take(2 * (nwg + 1) * (K + 1));
+  const int tid = threadIdx.x, wid = tid >> 5;
+  FOR_MN(i, l, mp, K) Us[i + l * lus] = i < m ? U[i + (int64_t)l * ldu] : 0.0;
+  FOR_MN(i, l, np_, K) Vs[i + l * lvs] = i < n ? V[i + (int64_t)l * ldv] : 0.0;
+  __syncthreads();
+  if (wid < nwg) {
+    if (K <= 32) ws_qr<1, HMX_WARPS / 2>(m, K, Us, lus, tpu, wdu, xchu, 0, 1);
+    else ws_qr<2, HMX_WARPS / 2>(m, K, Us, lus, tpu, wdu, xchu, 0, 1);
+  } else {
+    if (K <= 32) ws_qr<1, HMX_WARPS / 2>(n, K, Vs, lvs, tpv, wdv, xchv, nwg, 2);
+    else ws_qr<2, HMX_WARPS / 2>(n, K, Vs, lvs, tpv, wdv, xchv, nwg, 2);
+  }
+  __syncthreads();
+  FOR_MN(i, j, p, q) {
+    const int l0 = max(i, j);
+    w.G[i + j * lg] = ws_dot<4>(Us + i + l0 * lus, lus, Vs + j + l0 * lvs, lvs, K - l0);
+  }
+  __syncthreads();
+  // R_u, R_v are dead: striu(W^T W) of both factors replaces them (on the
+  // warps the pivoted QR does not use)
+  w.nsm = 2;
+  w.sA[0] = Us; w.swd[0] = wdu; w.sld[0] = lus; w.srows[0] = m; w.sp[0] = p;
+  w.sA[1] = Vs; w.swd[1] = wdv; w.sld[1] = lvs; w.srows[1] = n; w.sp[1] = q;
+  phase(P, 12, tq);
+  int k = 0;
+  const int r = ws_core(P, o, p, q, w, sm, tq, &k);
+  if (r > 0) {
+    const int gt = nwg * 32;
+    if (wid < nwg) {  // U' = Q_u [Yu; 0]
+      ws_wtb(p, p, Us, lus, wdu, w.Yu, ly, nullptr, r, w.Bu, ly, tid, gt);
+      named_bar(1, gt);
+      ws_trsolve(p, Us, lus, tpu, w.Bu, ly, r, tid, gt);
+      named_bar(1, gt);
+      ws_wz(m, p, Us, lus, wdu, w.Yu, ly, nullptr, p, w.Bu, ly, r, Uo, lduo, tid, gt);
+    } else {          // V' = Q_v [W'; 0]
+      const int t2 = tid - gt;
+      ws_wtb(q, q, Vs, lvs, wdv, w.X, lx, w.ord, r, Bv, lx, t2, gt);
+      named_bar(2, gt);
+      ws_trsolve(q, Vs, lvs, tpv, Bv, lx, r, t2, gt);
+      named_bar(2, gt);
+      ws_wz(n, q, Vs, lvs, wdv, w.X, lx, w.ord, q, Bv, lx, r, Vo, ldvo, t2, gt);
+    }
+  }
+  __syncthreads();
+  phase(P, 15, tq);
+  if (tid == 0) *rslot = r;
+  count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) + 2.0 * m * p * r +
+               2.0 * n * q * r,
+        8.0 * (2.0 * m * K + 2.0 * n * K + (double)K * K + (m + n) * (double)r));
+  __syncthreads();
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Panel (TSQR) truncation for factors that do not fit shared memory.  Each
+// factor is cut into row panels; a panel is factored in shared memory by
+// all warps (ws_qr), its R goes to the next level's stack, striu(W^T W)
+// replaces it and the panel returns to global memory in place.  Levels
+// repeat until one panel is left.  Q is applied top level first, each panel
+// with the three dense phases of hmx_ws.cuh.
+// ---------------------------------------------------------------------------
+constexpr int WS_MAXLEV = 4;
+struct WsLevels {
+  int L;                    // number of levels
+  int rows[WS_MAXLEV];      // rows of the level's matrix
+  int nb[WS_MAXLEV];        // panels
+  int pr[WS_MAXLEV];        // rows per panel (last one: the rest)
+  int64_t off[WS_MAXLEV];   // offset of the level's matrix in `big` (levels >= 1)
+  int sc0[WS_MAXLEV];       // index of the level's first panel in the scalar arrays
+  int64_t ybuf[2];          // ping-pong Y buffers in `big`
+  int64_t big_need;
+  int npanels;
+};
+
+// Panel structure of an M x K factor; false if unsupported.
+__device__ bool ws_levels(int M, int K, int pmax, WsLevels& lv) {
+  lv.L = 0;
+  lv.npanels = 0;
+  int rows = M;
+  int64_t off = 0;
+  for (;;) {
+    if (lv.L >= WS_MAXLEV) return false;
+    const int l = lv.L++;
+    lv.rows[l] = rows;
+    lv.off[l] = off;
+    lv.sc0[l] = lv.npanels;
+    if (rows <= pmax) {
+      lv.nb[l] = 1;
+      lv.pr[l] = rows;
+      lv.npanels += 1;
+      break;
+    }
+    const int nb = (rows + pmax - 1) / pmax;
+    const int pr = (((rows + nb - 1) / nb) + 7) & ~7;
+    const int last = rows - (nb - 1) * pr;
+    if (pr > pmax || pr < 4 * K || last < K) return false;
+    lv.nb[l] = nb;
+    lv.pr[l] = pr;
+    lv.npanels += nb;
+    if (l > 0) off += (int64_t)rows * K;
+    rows = nb * K;
+    if (l == 0) off = 0;
+  }
+  // level l >= 1 matrices are stored one after another in `big`
+  int64_t o2 = 0;
+  for (int l = 1; l < lv.L; ++l) { lv.off[l] = o2; o2 += (int64_t)lv.rows[l] * K; }
+  const int64_t yb = lv.L > 1 ? (int64_t)lv.rows[1] * K : 0;
+  lv.ybuf[0] = o2;
+  lv.ybuf[1] = o2 + yb;
+  lv.big_need = o2 + 2 * yb;
+  return true;
+}
+
+// Global -> shared copy of a rows x cols block (rows..rp-1 zero filled), four
+// independent loads in flight per thread before their stores.
+__device__ void ws_stage(int rows, int rp, int cols, const double* src, int lds, double* dst, int ldd) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = w; c < cols; c += HMX_WARPS) {
+    const double* s_ = src + (int64_t)c * lds;
+    double* d_ = dst + c * ldd;
+    for (int i = lane; i < rp; i += 128) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (i + 32 * u < rows) ? s_[i + 32 * u] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) if (i + 32 * u < rp) d_[i + 32 * u] = v[u];
+    }
+  }
+}
+
+// QR of every level of one factor.  A: the factor (global, in place).
+// Rz (p x K, ld p): the final R.  scal: tp/wd of every panel (2K each).
+__device__ void ws_panel_qr(const WsLevels& lv, int K, double* A, int lda, double* big, double* Rz,
+                            double* scal, double* wk) {
+  const int tid = threadIdx.x;
+  for (int l = 0; l < lv.L; ++l) {
+    double* Al = l == 0 ? A : big + lv.off[l];
+    const int ldl = l == 0 ? lda : lv.rows[l];
+    for (int b = 0; b < lv.nb[l]; ++b) {
+      const int i0 = b * lv.pr[l];
+      const int rows = min(lv.pr[l], lv.rows[l] - i0);
+      const int rp = ws_qr_rows(rows, HMX_WARPS, K <= 32 ? 1 : (K <= 64 ? 2 : 4));
+      const int lp = rp | 1;
+      double* Ps = wk;
+      double* tps = Ps + (int64_t)lp * K;
+      double* wds = tps + K;
+      double* xch = wds + K;
+      double* Ag = Al + i0;
+      ws_stage(rows, rp, K, Ag, ldl, Ps, lp);
+      __syncthreads();
+      if (K <= 32) ws_qr<1, HMX_WARPS>(rows, K, Ps, lp, tps, wds, xch, 0, 0);
+      else if (K <= 64) ws_qr<2, HMX_WARPS>(rows, K, Ps, lp, tps, wds, xch, 0, 0);
+      else ws_qr<4, HMX_WARPS>(rows, K, Ps, lp, tps, wds, xch, 0, 0);
+      const int pb = min(rows, K);
+      if (l + 1 < lv.L) {  // R block b of the next level's stack
+        double* Sn = big + lv.off[l + 1] + (int64_t)b * K;
+        const int lds = lv.rows[l + 1];
+        FOR_MN(i, c, pb, K) Sn[i + (int64_t)c * lds] = (c >= i) ? Ps[i + c * lp] : 0.0;
+      } else {
+        FOR_MN(i, c, pb, K) Rz[i + (int64_t)c * pb] = (c >= i) ? Ps[i + c * lp] : 0.0;
+      }
+      __syncthreads();
+      ws_smat(rows, pb, Ps, lp, wds, tid, HMX_THREADS);
+      __syncthreads();
+      FOR_MN(i, c, rows, K) Ag[i + (int64_t)c * ldl] = Ps[i + c * lp];
+      double* sc = scal + (int64_t)(lv.sc0[l] + b) * 2 * K;
+      for (int e = tid; e < pb; e += HMX_THREADS) { sc[e] = tps[e]; sc[K + e] = wds[e]; }
+      __syncthreads();
+    }
+  }
+}
+
+// Out (M x r, ld ldo) = Q [Yin; 0] for a factor held as panels.  Yin: p x r
+// in shared memory (column t at Yin + ymap[t] * ldy).  T: (K|1) x K staging
+// of a panel's top block, Ys / B: (K|1) x r each, sc: 2K doubles (all
+// shared memory).
+__device__ void ws_panel_apply(const WsLevels& lv, int K, const double* A, int lda, double* big,
+                               const double* scal, const double* Yin, int ldy, const int* ymap, int r,
+                               double* T, double* Ys, double* B, double* sc, double* Out, int ldo) {
+  const int tid = threadIdx.x;
+  const int lk = K | 1;
+  for (int l = lv.L - 1; l >= 0; --l) {
+    const double* Al = l == 0 ? A : big + lv.off[l];
+    const int ldl = l == 0 ? lda : lv.rows[l];
+    const bool top = (l == lv.L - 1);
+    // input of this level: Yin (top) or the previous level's output
+    const double* Yprev = top ? nullptr : big + lv.ybuf[(l + 1) & 1];
+    const int ldprev = top ? 0 : lv.rows[l + 1];
+    double* Ol = l == 0 ? Out : big + lv.ybuf[l & 1];
+    const int ldol = l == 0 ? ldo : lv.rows[l];
+    for (int b = 0; b < lv.nb[l]; ++b) {
+      const int i0 = b * lv.pr[l];
+      const int rows = min(lv.pr[l], lv.rows[l] - i0);
+      const int pb = min(rows, K);
+      const double* Ag = Al + i0;
+      const double* scg = scal + (int64_t)(lv.sc0[l] + b) * 2 * K;
+      FOR_MN(i, c, pb, pb) T[i + c * lk] = Ag[i + (int64_t)c * ldl];
+      for (int e = tid; e < pb; e += HMX_THREADS) { sc[e] = scg[e]; sc[K + e] = scg[K + e]; }
+      const double* Y = Yin;
+      int ly = ldy;
+      const int* ym = ymap;
+      if (!top) {
+        FOR_MN(i, t, K, r) Ys[i + t * lk] = Yprev[(int64_t)b * K + i + (int64_t)t * ldprev];
+        Y = Ys; ly = lk; ym = nullptr;
+      }
+      __syncthreads();
+      ws_wtb(pb, pb, T, lk, sc + K, Y, ly, ym, r, B, lk, tid, HMX_THREADS);
+      __syncthreads();
+      ws_trsolve(pb, T, lk, sc, B, lk, r, tid, HMX_THREADS);
+      __syncthreads();
+      ws_wz(rows, pb, Ag, ldl, sc + K, Y, ly, ym, pb, B, lk, r, Ol + i0, ldol, tid, HMX_THREADS, true);
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __noinline__ bool trunc_ws_panel(const DevPlan& P, const hmx_op& o, int m, int n, int K,
+                                            double* U, int ldu, double* V, int ldv, double* Uo, int lduo,
+                                            double* Vo, int ldvo, int* rslot, double* ws, int64_t kb,
+                                            double* sm, unsigned long long& tq) {
+  const int p = min(m, K), q = min(n, K), s = min(p, q);
+  if (K > 128 || q > 128) return false;
+  const int lg = p | 1, lx = q | 1, ly = p | 1, lk = K | 1;
+  // core phase: G (aliased by the panel top block T), X, Yu, Bu + arrays
+  const int64_t gsz = max((int64_t)lg * q, (int64_t)lk * K);
+  const int64_t ysz = max((int64_t)ly * s, (int64_t)lk * s);
+  const int64_t core_need = gsz + (int64_t)lg * s + (int64_t)lx * s + 2 * ysz + 10 * (int64_t)K + 64;
+  if (core_need > P.smem_work) return false;
+  const int pmax = (int)(((int64_t)P.smem_work - 2 * (HMX_WARPS + 1) * (K + 1) - 2 * K - 64) / K - 1) & ~63;
+  if (pmax < K) return false;
+  WsLevels lu, lv;
+  if (!ws_levels(m, K, pmax, lu) || !ws_levels(n, K, pmax, lv)) return false;
+  // global workspace (planner: 5 kb^2 + (m + n + 200) kb + 2048 doubles)
+  double* Rzu = ws;
+  double* Rzv = ws + kb * kb;
+  double* scal = ws + 2 * kb * kb;
+  const int64_t scal_cap = 3 * kb * kb;
+  if ((int64_t)(lu.npanels + lv.npanels) * 2 * K > scal_cap) return false;
+  double* bigu = ws + 5 * kb * kb;
+  double* bigv = bigu + (int64_t)m * kb + 97 * kb + 1024;
+  if (lu.big_need > (int64_t)m * kb + 97 * kb + 1024 || lv.big_need > (int64_t)n * kb + 97 * kb + 1024)
+    return false;
+  double* scu = scal;
+  double* scv = scal + (int64_t)lu.npanels * 2 * K;
+  const int tid = threadIdx.x;
+  double* wk = sm + 32;
+  ws_panel_qr(lu, K, U, ldu, bigu, Rzu, scu, wk);
+  ws_panel_qr(lv, K, V, ldv, bigv, Rzv, scv, wk);
+  double* wp = wk;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
+  WsCore w;
+  w.lg = lg; w.lx = lx; w.ly = ly; w.lwc = lg; w.late = false;
+  w.G = take(gsz);
+  w.Wc = take((int64_t)lg * s);
+  w.X = take((int64_t)lx * s);
+  w.Yu = take(ysz);
+  w.Bu = take(ysz);
+  w.tpg = take(K); w.wdg = take(K); w.rdg = take(K); w.sig = take(K);
+  w.perm = reinterpret_cast<int*>(take(K));
+  w.pos = w.perm + K;
+  w.ord = reinterpret_cast<int*>(take(K));
+  w.xr = take(32);
+  double* sc = take(2 * K);
+  w.nsm = 0;
+  FOR_MN(i, j, p, q) {
+    const int l0 = max(i, j);
+    w.G[i + j * lg] = ws_dot<4>(Rzu + i + (int64_t)l0 * p, p, Rzv + j + (int64_t)l0 * q, q, K - l0);
+  }
+  __syncthreads();
+  phase(P, 12, tq);
+  int k = 0;
+  const int r = ws_core(P, o, p, q, w, sm, tq, &k);
+  if (r > 0) {
+    // G is dead after ws_core: its storage stages the panels' top blocks.
+    // The top level reads Yu / X directly and uses Bu; lower levels stage
+    // their input in the Yu storage (dead after the top level of U; V's top
+    // level reads X).
+    ws_panel_apply(lu, K, U, ldu, bigu, scu, w.Yu, ly, nullptr, r, w.G, w.Yu, w.Bu, sc, Uo, lduo);
+    ws_panel_apply(lv, K, V, ldv, bigv, scv, w.X, lx, w.ord, r, w.G, w.Yu, w.Bu, sc, Vo, ldvo);
+  }
+  __syncthreads();
+  phase(P, 15, tq);
+  if (tid == 0) *rslot = r;
+  count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) + 2.0 * m * p * r +
+               2.0 * n * q * r,
+        8.0 * (2.0 * m * K + 2.0 * n * K + (double)K * K + (m + n) * (double)r));
+  __syncthreads();
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // truncate (hmatrix.py:113-130): QR(U), QR(V), SVD(Ru Rv^T), keep, recompose
 // ---------------------------------------------------------------------------
@@ -323,6 +779,12 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   double* red = sm;
   double* work = sm + 32;
   const int p = min(m, K), q = min(n, K);
+#if HMX_WS
+  if (trunc_ws_small(P, o, m, n, K, U, ldu, V, ldv, Uo, lduo, Vo, ldvo, rslot, sm, tq)) return;
+#if HMX_WS > 1
+  if (trunc_ws_panel(P, o, m, n, K, U, ldu, V, ldv, Uo, lduo, Vo, ldvo, rslot, ws, kb, sm, tq)) return;
+#endif
+#endif
   // stage U, V (and G) in shared memory when they fit
   const int ms = m, ns = n, pg = p;
   const int64_t need = (int64_t)(ms + ns) * K + 2 * K + (int64_t)pg * q;
@@ -411,6 +873,50 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
 // ---------------------------------------------------------------------------
 // dense_to_lowrank (hmatrix.py:133-138)
 // ---------------------------------------------------------------------------
+// dense_to_lowrank on the warp-synchronous core: the block is staged in
+// shared memory, pivoted QR + Jacobi + Q_G as in the truncation; M stays
+// intact, so a block whose revealed rank does not fit falls back (false).
+__device__ __noinline__ bool d2lr_ws(const DevPlan& P, const hmx_op& o, int m, int n, const double* M,
+                                     int ldm, double* Uo, int lduo, double* Vo, int ldvo, int* rslot,
+                                     double* ws, double* sm) {
+  if (n > 128 || m > 256) return false;
+  const int lg = m | 1, lx = n | 1, ly = m | 1;
+  const int64_t fixed = (int64_t)lg * n + 8 * (int64_t)n + 96;
+  if (fixed + (int64_t)(lg + lx + 2 * ly) > P.smem_work) return false;
+  double* wp = sm + 32;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
+  WsCore w;
+  w.lg = lg; w.lx = lx; w.ly = ly; w.lwc = lg;
+  w.tpg = take(n); w.wdg = take(n); w.rdg = take(n); w.sig = take(n);
+  w.perm = reinterpret_cast<int*>(take(n));
+  w.pos = w.perm + n;
+  w.ord = reinterpret_cast<int*>(take(n));
+  w.xr = take(32);
+  w.G = take((int64_t)lg * n);
+  w.nsm = 0;
+  w.late = true;
+  w.free2 = wp;
+  w.cap2 = (int64_t)P.smem_work - (wp - (sm + 32));
+  const int l = max(m, n);
+  w.gev = ws + 8 * l;  // the planner's 2 l^2 doubles
+  w.ldev = m;
+  FOR_MN(i, j, m, n) w.G[i + j * lg] = M[i + (int64_t)j * ldm];
+  __syncthreads();
+  unsigned long long tq = P.trace ? gtimer2() : 0;
+  int k = 0;
+  const int r = ws_core(P, o, m, n, w, sm, tq, &k);
+  if (r < 0) return false;
+  FOR_MN(i, t, m, r) Uo[i + (int64_t)t * lduo] = w.Yu[i + t * ly];
+  FOR_MN(c_, t, n, r) Vo[c_ + (int64_t)t * ldvo] = w.X[c_ + (int64_t)w.ord[t] * lx];
+  __syncthreads();
+  phase(P, 15, tq);
+  if (threadIdx.x == 0) *rslot = r;
+  const int s_ = min(m, n);
+  count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s_ + (double)s_ * n));
+  __syncthreads();
+  return true;
+}
+
 __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* sm) {
   const int m = o.dim[0], n = o.dim[1];
   int* rslot = slotp(P, c, o.slot[0]);
@@ -420,6 +926,9 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* Uo = mref(P, c, o.ref[2]);
   double* Vo = mref(P, c, o.ref[3]);
   double* ws = mref(P, c, o.wref);
+#if HMX_WS
+  if (d2lr_ws(P, o, m, n, M, ldm, Uo, o.ld[2], Vo, o.ld[3], rslot, ws, sm)) return;
+#endif
   double* work = sm + 32;
   double* G = M;
   int ldg = ldm;
