@@ -22,10 +22,12 @@ leaves.  A failed check prints ``value: null`` with the reason.
                                          in oracle/hm_oracle.py, on the same
                                          config, assembled on the CPU)
 
-Under torchrun (N>1): c4 shards its 256 instances over the ranks (no
-collective on the data path); the other configs run one independent
-factorization per rank (replicas; the partitioned multi-GPU runner is not
-built).  Time is the max over ranks of the device time.
+Under torchrun (N>1): the single-matrix configs run ONE factorization
+partitioned over the ranks by block rows (run_partitioned: strong scaling,
+partition.DistributedHLU); c4 shards its 256 instances over the ranks (no
+collective on the data path).  HMX_BENCH_REPLICAS=1: one independent
+factorization per rank instead.  Time is the max over ranks of the device
+time.
 """
 
 from __future__ import annotations
@@ -441,7 +443,106 @@ def main():
         return run_reference(args)
     if args.config == "c4":
         return run_c4(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not os.environ.get("HMX_BENCH_REPLICAS"):
+        return run_partitioned(args)
     return run_single(args)
+
+
+def run_partitioned(args):
+    """N > 1: ONE factorization of the config matrix partitioned over the
+    ranks by block rows (partition.DistributedHLU: peer-memory exchange along
+    DAG edges, no collective on the data path).  Strong scaling: the total
+    work is fixed.  HMX_BENCH_REPLICAS=1 restores one matrix per GPU."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1911_07531_b200 import hmatrix as H
+    from paper_1911_07531_b200.partition import DistributedHLU
+
+    rc = rank_cap_of(args.config, args.rank_cap)
+    cfg, broot, pol, A0, setup = build_case(args.config, rc)
+    mode = args.mode or cfg.mode
+    t0 = time.time()
+    d = DistributedHLU(A0.table, mode, pol, rc)
+    setup["plan_s"] = time.time() - t0
+    A, L, U = d.stores(A0.store)
+    d.connect(A, L, U)
+    clk = ClockSampler(local)
+
+    def one():
+        A.copy_from(A0.store)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d.run(events=(e0, e1))
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        one()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with clk:
+        per_step = [one() for _ in range(args.steps)]
+    dist.barrier()
+    tt = torch.tensor([float(np.mean(per_step))], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    c = d.pp.plan.counters()
+    cc = torch.tensor([float(c[1]), float(c[2]), float(c[0])], device="cuda", dtype=torch.float64)
+    dist.all_reduce(cc)
+    flops, alg_bytes, ntrunc = (float(x) for x in cc.tolist())
+    Lf, Uf = d.collect(L, 1), d.collect(U, 2)
+    st = d.part.stats()
+    d.close()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    Lh, Uh = H.HMatrix(Lf, 0, pol), H.HMatrix(Uf, 0, pol)
+    par, ok = ({"skipped": True}, True) if args.no_parity else parity_report(cfg, mode, Lh, Uh)
+    peaks = fp64_peaks(torch)
+    hbm, hbm_src = hbm_peak()
+    value = flops / (t_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value if ok else None, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS.get(cfg.name, cfg.name), "n": int(cfg.n), "mode": mode,
+                   "executor": "persistent (one launch per rank, ranks release each other's tasks)",
+                   "rank_cap": rc,
+                   "step": "one H-LU factorization of the config matrix partitioned over the ranks",
+                   "parallelism": f"block-row partition x{world} (peer-memory exchange along DAG edges)",
+                   "partition": st},
+        "factor_time_s": t_ms * 1e-3,
+        "factor_time_steps_s": [x * 1e-3 for x in per_step],
+        "gflop_per_factorization": flops / 1e9,
+        "truncations": int(ntrunc),
+        "parity": par,
+        "roofline": {"bound": "tensor", "achieved": value / 1e3, "peak": world * peaks["dgemm_tflops"],
+                     "unit": "TFLOP/s", "frac": value / 1e3 / (world * peaks["dgemm_tflops"]),
+                     "traffic": None,
+                     "peak_source": "FP64: torch/cuBLAS DGEMM 8192^3 measured in this run, x n_gpus",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "hbm_achieved_gbs": alg_bytes / (t_ms * 1e-3) / 1e9, "hbm_peak_gbs": world * hbm,
+                     "hbm_peak_source": hbm_src,
+                     "kernel": "k_persistent<1> (one launch per rank = its share of one factorization)"},
+        "cpu_baseline": None,
+        "e2e": None,
+        "gpu_launches": args.steps * world,
+        "clocks": clk.summary(),
+        "setup": setup,
+    }
+    if not ok:
+        line["value_withheld"] = "factors failed the parity check against the reference fixture"
+        line["value_unchecked"] = value
+    print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 def run_single(args):

@@ -502,8 +502,9 @@ class DistributedHLU:
         self._connected = True
         self.dist.barrier(group=self.group)
 
-    def run(self, stream=None, check=True):
-        """One factorization.  Every rank resets its own scheduler state
+    def run(self, stream=None, check=True, events=None):
+        """One factorization (events: optional (start, end) CUDA events
+        recorded around this rank's launch).  Every rank resets its own scheduler state
         BEFORE the barrier: a peer may release tasks of this rank as soon as
         it starts, so no rank may launch while another still resets."""
         if not self._connected:
@@ -513,7 +514,11 @@ class DistributedHLU:
         plan.reset(stream)
         self.backend.synchronize()
         self.dist.barrier(group=self.group)
+        if events is not None:
+            events[0].record(stream)
         plan.execute(4, stream)
+        if events is not None:
+            events[1].record(stream)
         if check:
             self.pp.check(stream)
         self.dist.barrier(group=self.group)
