@@ -57,8 +57,13 @@ constexpr int kScratchBase = 15;
 // High-occupancy variant: 2 CTAs/SM of 256 threads, or 4 of 128 threads
 // when built with -DHMX_THREADS=128 (experiments).
 constexpr int OCC_HI = HMX_THREADS == 128 ? 4 : 2;
+// 1 CTA/SM: nearly all of the 227 KB a block may own (the truncation paths
+// are shared-memory resident; ~29 KB of L1 remain for the streaming ops)
+#ifndef HMX_SMEM1
+#define HMX_SMEM1 28928
+#endif
 __host__ __device__ constexpr int smem_doubles(int occ) {
-  return occ == 1 ? 20480 : (occ == 2 ? 14080 : 7040);
+  return occ == 1 ? HMX_SMEM1 : (occ == 2 ? 14080 : 7040);
 }
 
 struct DevPlan {
@@ -288,7 +293,7 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
 }
 
 #ifndef HMX_WS
-#define HMX_WS 2  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path
+#define HMX_WS 3  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path, 3: + fat path
 #endif
 
 // Core of both warp-synchronous truncation paths, after G (p x q, shared
@@ -404,6 +409,8 @@ __device__ __noinline__ int ws_core(const DevPlan& P, const hmx_op& o, int p, in
   }
   ws_smat(p, k, w.Wc, w.lwc, w.wdg, tid, HMX_THREADS);
   __syncthreads();
+  // R1 is consumed and the tails sit in Wc: G's storage becomes Bu
+  if (!w.late) w.Bu = w.G;
   // kept columns of X become W' = X / sigma;  Yu := Q_G Yu
   for (int e = tid; e < q * r; e += HMX_THREADS) {
     const int c = e % q, col = w.ord[e / q];
@@ -430,7 +437,7 @@ __device__ __noinline__ bool trunc_ws_small(const DevPlan& P, const hmx_op& o, i
   const int mp = ws_qr_rows(m, nwg, ct), np_ = ws_qr_rows(n, nwg, ct);  // zero-padded row counts
   const int lus = mp | 1, lvs = np_ | 1, lg = p | 1, lx = q | 1, ly = p | 1;
   const int64_t need = (int64_t)(lus + lvs) * K + (int64_t)lg * q + (int64_t)lg * s + (int64_t)lx * s +
-                       2 * (int64_t)ly * s + (int64_t)lx * s + 12 * K + 4 * (nwg + 1) * (K + 1) + 64;
+                       (int64_t)ly * s + (int64_t)lx * s + 12 * K + 4 * (nwg + 1) * (K + 1) + 64;
   if (need > P.smem_work) return false;
   double* wp = sm + 32;
   auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
@@ -442,7 +449,7 @@ __device__ __noinline__ bool trunc_ws_small(const DevPlan& P, const hmx_op& o, i
   w.Wc = take((int64_t)lg * s);
   w.X = take((int64_t)lx * s);
   w.Yu = take((int64_t)ly * s);
-  w.Bu = take((int64_t)ly * s);
+  w.Bu = nullptr;  // G's storage once R1 is consumed (ws_core)
   double* Bv = take((int64_t)lx * s);
   double* tpu = take(K); double* wdu = take(K);
   double* tpv = take(K); double* wdv = take(K);
@@ -671,14 +678,15 @@ __device__ void ws_panel_apply(const WsLevels& lv, int K, const double* A, int l
 __device__ __noinline__ bool trunc_ws_panel(const DevPlan& P, const hmx_op& o, int m, int n, int K,
                                             double* U, int ldu, double* V, int ldv, double* Uo, int lduo,
                                             double* Vo, int ldvo, int* rslot, double* ws, int64_t kb,
-                                            double* sm, unsigned long long& tq) {
+                                            double* sm, unsigned long long& tq, bool counted = true) {
   const int p = min(m, K), q = min(n, K), s = min(p, q);
   if (K > 128 || q > 128) return false;
   const int lg = p | 1, lx = q | 1, ly = p | 1, lk = K | 1;
   // core phase: G (aliased by the panel top block T), X, Yu, Bu + arrays
   const int64_t gsz = max((int64_t)lg * q, (int64_t)lk * K);
   const int64_t ysz = max((int64_t)ly * s, (int64_t)lk * s);
-  const int64_t core_need = gsz + (int64_t)lg * s + (int64_t)lx * s + 2 * ysz + 10 * (int64_t)K + 64;
+  const int64_t wsz = max((int64_t)lg * s, (int64_t)lk * K);
+  const int64_t core_need = gsz + wsz + (int64_t)lx * s + ysz + 10 * (int64_t)K + 64;
   if (core_need > P.smem_work) return false;
   const int pmax = (int)(((int64_t)P.smem_work - 2 * (HMX_WARPS + 1) * (K + 1) - 2 * K - 64) / K - 1) & ~63;
   if (pmax < K) return false;
@@ -705,10 +713,10 @@ __device__ __noinline__ bool trunc_ws_panel(const DevPlan& P, const hmx_op& o, i
   WsCore w;
   w.lg = lg; w.lx = lx; w.ly = ly; w.lwc = lg; w.late = false;
   w.G = take(gsz);
-  w.Wc = take((int64_t)lg * s);
+  w.Wc = take(wsz);
   w.X = take((int64_t)lx * s);
   w.Yu = take(ysz);
-  w.Bu = take(ysz);
+  w.Bu = nullptr;  // G's storage once R1 is consumed (ws_core)
   w.tpg = take(K); w.wdg = take(K); w.rdg = take(K); w.sig = take(K);
   w.perm = reinterpret_cast<int*>(take(K));
   w.pos = w.perm + K;
@@ -725,19 +733,282 @@ __device__ __noinline__ bool trunc_ws_panel(const DevPlan& P, const hmx_op& o, i
   int k = 0;
   const int r = ws_core(P, o, p, q, w, sm, tq, &k);
   if (r > 0) {
-    // G is dead after ws_core: its storage stages the panels' top blocks.
-    // The top level reads Yu / X directly and uses Bu; lower levels stage
+    // After ws_core G's storage is Bu and Wc is dead: Wc stages the panels'
+    // top blocks.  The top level reads Yu / X directly; lower levels stage
     // their input in the Yu storage (dead after the top level of U; V's top
     // level reads X).
-    ws_panel_apply(lu, K, U, ldu, bigu, scu, w.Yu, ly, nullptr, r, w.G, w.Yu, w.Bu, sc, Uo, lduo);
-    ws_panel_apply(lv, K, V, ldv, bigv, scv, w.X, lx, w.ord, r, w.G, w.Yu, w.Bu, sc, Vo, ldvo);
+    ws_panel_apply(lu, K, U, ldu, bigu, scu, w.Yu, ly, nullptr, r, w.Wc, w.Yu, w.Bu, sc, Uo, lduo);
+    ws_panel_apply(lv, K, V, ldv, bigv, scv, w.X, lx, w.ord, r, w.Wc, w.Yu, w.Bu, sc, Vo, ldvo);
   }
   __syncthreads();
+  phase(P, 15, tq);
+  if (tid == 0) *rslot = r;
+  if (counted)
+    count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) + 2.0 * m * p * r +
+                 2.0 * n * q * r,
+          8.0 * (2.0 * m * K + 2.0 * n * K + (double)K * K + (m + n) * (double)r));
+  __syncthreads();
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// "Fat" truncation: factors with up to 128 columns whose QR does not fit
+// the shared-memory paths.  One side of the product is either a factor in
+// global memory, factored by the column-blocked QR (ws_cbqr), or an already
+// orthonormal factor given by its reflectors (dense_to_lowrank: Q_G of the
+// pivoted QR, R = I).  The core G (p x q <= 128 x 128) is factored in shared
+// memory (pivoted QR, Jacobi on R1^T); everything of size p x k lives in
+// global scratch (L2) and is applied block-wise (ws_apply_block).
+// ---------------------------------------------------------------------------
+struct FatSide {
+  int rows, p;          // rows of the factor, number of reflectors
+  const double* A;      // clean reflector blocks (tails, wd on the diagonal, zeros above), global
+  int64_t lda;
+  const double* tp;     // p scalars
+  const double* Sg;     // striu(W_c^T W_c) of block c at Sg + c * lds * lds (ld lds)
+  int lds;
+  int nb;               // block width (single block: nb >= p)
+};
+
+// Out (rows x r) = Q [Yin; 0]
+__device__ void fat_apply(const FatSide& f, const double* Yin, int64_t ldy, int r, double* Out, int64_t ldo,
+                          double* Sc, double* Bm, double* sw, double* gsm) {
+  FOR_MN(i, t, f.rows, r) Out[i + (int64_t)t * ldo] = i < f.p ? Yin[i + (int64_t)t * ldy] : 0.0;
+  __syncthreads();
+  const int nblk = (f.p + f.nb - 1) / f.nb;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int c0 = b * f.nb, jc = min(f.nb, f.p - c0);
+    ws_apply_block(f.rows - c0, jc, f.A + c0 + (int64_t)c0 * f.lda, f.lda, f.tp + c0,
+                   f.Sg + (int64_t)b * f.lds * f.lds, f.lds, false, Out + c0, ldo, r, Sc, Bm, sw, gsm);
+  }
+}
+
+// shared work the fat core needs (doubles) for a p x q core, block widths
+// nbu / nbv of the outer factors, rank cap rcap
+__device__ __forceinline__ int64_t fat_core_need(int p, int q, int nbu, int nbv, int rcap) {
+  const int l = max(p, q), s = min(p, q);
+  const int nbw = max(max(nbu, nbv), s);
+  const int64_t a = (int64_t)(l | 1) * l;  // G / X
+  const int64_t b = (int64_t)(nbw | 1) * nbw + (int64_t)(nbw | 1) * rcap + nbw + GEMM_SMEM_DOUBLES;  // Sc, Bm, sw, gsm
+  return max(a, b) + 7 * (int64_t)q + 96;
+}
+
+// Core and recomposition.  Ru (p x Kc, ld p) and Rv (q x Kc, ld q) in global
+// (Ru == nullptr: the identity, p == Kc).  gs: global scratch of at least
+// 6 max(p,q)^2 + 2 max(p,q) doubles.  Returns r; Uo / Vo written.
+__device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc, const double* Ru,
+                        const double* Rv, const FatSide& fu, const FatSide& fv, double* Uo, int lduo,
+                        double* Vo, int ldvo, double* gs, double* sm, unsigned long long& tq) {
+  int* ired = reinterpret_cast<int*>(sm + 16);
+  int* flag = reinterpret_cast<int*>(sm + 24);
+  const int tid = threadIdx.x;
+  const int l = max(p, q);
+  const int lg = p | 1, lx = q | 1;
+  double* wp = sm + 32;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
+  double* tpg = take(q); double* wdg = take(q); double* rdg = take(q); double* sig = take(q);
+  int* perm = reinterpret_cast<int*>(take(q));
+  int* pos = perm + q;
+  int* ord = reinterpret_cast<int*>(take(q));
+  double* xr = take(32);
+  double* big = wp;  // G, then X, then the block-apply work (Sc, Bm, sw, gsm)
+  double* G = big;
+  FOR_MN(i, j, p, q) {
+    const int l0 = max(i, j);
+    G[i + j * lg] = Ru ? ws_dot<4>(Ru + i + (int64_t)l0 * p, p, Rv + j + (int64_t)l0 * q, q, Kc - l0)
+                       : (i >= j ? Rv[j + (int64_t)i * q] : 0.0);  // Ru = I: G = Rv^T (lower triangular)
+  }
+  __syncthreads();
+  phase(P, 12, tq);
+  const int policy = o.iarg[0];
+  const double cut = (policy == 2) ? o.farg[1] : 1e-14;
+  const double thr = HMX_RRQR_THR * cut;
+  const int nwr = (q + 31) >> 5;
+  if ((tid >> 5) < nwr) {
+    const int k = ws_rrqr(p, q, G, lg, tpg, wdg, rdg, perm, pos, thr, xr, 0, nwr, 3);
+    if (tid == 0) ired[0] = k;
+  }
+  __syncthreads();
+  const int k = ired[0];
+  phase(P, 13, tq);
+  // global scratch
+  const int64_t l2 = (int64_t)l * l;
+  double* X0 = gs;              // q x k (ld q): R1^T before the rotations
+  double* Yu = X0 + l2;         // p x r (ld p)
+  double* Yv = Yu + l2;         // q x r (ld q)
+  double* Wc = Yv + l2;         // p x k (ld p): Q_G as one clean reflector block
+  double* Sq = Wc + l2;         // k x k (ld k): W_c^T W_c
+  double* Xs = Sq + l2;         // q x r (ld q): kept columns of X
+  double* tpq = Xs + l2;        // k
+  // the clean reflector block of Q_G and R1^T leave G before X takes its storage
+  FOR_MN(i, j, p, k) {
+    const int pc = perm[j];
+    Wc[i + (int64_t)j * p] = i > j ? G[i + pc * lg] : (i == j ? wdg[j] : 0.0);
+  }
+  FOR_MN(c, i, q, k) {
+    const int pc = pos[c];
+    X0[c + (int64_t)i * q] = pc > i ? G[i + c * lg] : (pc == i ? rdg[i] : 0.0);
+  }
+  for (int e = tid; e < k; e += HMX_THREADS) tpq[e] = tpg[e];
+  __syncthreads();
+  double* X = big;  // q x k (shared)
+  FOR_MN(c, i, q, k) X[c + i * lx] = X0[c + (int64_t)i * q];
+  __syncthreads();
+  int sweeps = 0;
+  if (k > 0 && !ws_jacobi(q, k, X, lx, sig, ord, flag, &sweeps))
+    if (tid == 0) set_status(P, HMX_ERR_NOT_CONVERGED);
+  phase(P, 14, tq, sweeps);
+  int r = keep_count(policy, o.iarg[1], o.farg[1], sig, ord, k);
+  const int cap = o.iarg[2];
+  if (r > cap) {
+    if (tid == 0) set_status(P, HMX_ERR_RANK_OVERFLOW);
+    r = cap;
+  }
+  if (r == 0) return 0;
+  // kept columns of X (unscaled) to global, then X's storage is the work area
+  FOR_MN(c, t, q, r) Xs[c + (int64_t)t * q] = X[c + (int64_t)ord[t] * lx];
+  __syncthreads();
+  const int nbw = max(max(min(fu.nb, fu.p), min(fv.nb, fv.p)), k);
+  double* Sc = big;
+  double* Bm = Sc + (int64_t)(nbw | 1) * nbw;
+  double* sw = Bm + (int64_t)(nbw | 1) * r;
+  double* gsm = sw + nbw;
+  // Yu_top = R1 Xs / sigma = X0^T Xs / sigma (k x r), rows k..p-1 zero; Yv = Xs / sigma
+  cta_gemm(k, r, q, 1.0, X0, q, true, Xs, q, false, false, Yu, p, gsm);
+  FOR_MN(i, t, p, r) {
+    const double sg = sig[ord[t]];
+    Yu[i + (int64_t)t * p] = i < k ? Yu[i + (int64_t)t * p] / sg : 0.0;
+  }
+  FOR_MN(c, t, q, r) Yv[c + (int64_t)t * q] = Xs[c + (int64_t)t * q] / sig[ord[t]];
+  ws_smat_gemm(p, k, Wc, p, Sq, k, gsm);
+  // Yu := Q_G Yu
+  ws_apply_block(p, k, Wc, p, tpq, Sq, k, false, Yu, p, r, Sc, Bm, sw, gsm);
+  fat_apply(fu, Yu, p, r, Uo, lduo, Sc, Bm, sw, gsm);
+  fat_apply(fv, Yv, q, r, Vo, ldvo, Sc, Bm, sw, gsm);
+  __syncthreads();
+  return r;
+}
+
+__device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int m, int n, int K, double* U,
+                                          int ldu, double* V, int ldv, double* Uo, int lduo, double* Vo,
+                                          int ldvo, int* rslot, double* ws, int64_t kb, double* sm,
+                                          unsigned long long& tq) {
+  const int p = min(m, K), q = min(n, K);
+  if (K > 128 || p > 128 || q > 128 || K < 8) return false;
+  const int nbu = ws_cb_nb(m, K, P.smem_work), nbv = ws_cb_nb(n, K, P.smem_work);
+  // tall factors would need many narrow column blocks, each re-applying all
+  // previous ones from global memory: they stay with the blocked path
+  if (nbu < min(32, (K + 7) & ~7) || nbv < min(32, (K + 7) & ~7)) return false;
+  const int rcap = min(min(p, q), max(o.iarg[2], 1));
+  if (fat_core_need(p, q, min(nbu, p), min(nbv, q), rcap) > P.smem_work) return false;
+  // global workspace (planner: 9 kb^2 + (m + n + 200) kb + 2048 doubles):
+  // R_u, R_v, tp (2 K), the per-block S of both factors (<= 2 * 128 K), fat_core's 6 l^2 + 2 l
+  const int64_t l = max(p, q);
+  if (kb < K || 2 * (int64_t)K * K + 2 * (int64_t)K + 256 * (int64_t)K + 6 * l * l + 2 * l >
+                    9 * kb * kb + 200 * kb + 2048)
+    return false;
+  double* Rzu = ws;
+  double* Rzv = Rzu + (int64_t)p * K;
+  double* tpu = Rzv + (int64_t)q * K;
+  double* tpv = tpu + K;
+  double* Sgu = tpv + K;
+  double* Sgv = Sgu + 128 * (int64_t)K;  // (ceil(p / nb) blocks of nb^2 <= (p + nb) nb)
+  double* gs = Sgv + 128 * (int64_t)K;
+  const int tid = threadIdx.x;
+  double* wk = sm + 32;
+  ws_cbqr(m, K, U, ldu, Rzu, tpu, Sgu, nbu, wk);
+  ws_cbqr(n, K, V, ldv, Rzv, tpv, Sgv, nbv, wk);
+  FatSide fu{m, p, U, ldu, tpu, Sgu, nbu, nbu};
+  FatSide fv{n, q, V, ldv, tpv, Sgv, nbv, nbv};
+  const int r = fat_core(P, o, p, q, K, Rzu, Rzv, fu, fv, Uo, lduo, Vo, ldvo, gs, sm, tq);
   phase(P, 15, tq);
   if (tid == 0) *rslot = r;
   count(P, qr_flops(m, K) + qr_flops(n, K) + 2.0 * p * q * K + svd_flops(p, q) + 2.0 * m * p * r +
                2.0 * n * q * r,
         8.0 * (2.0 * m * K + 2.0 * n * K + (double)K * K + (m + n) * (double)r));
+  __syncthreads();
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// dense_to_lowrank of a block too large for shared memory (<= 512 x 512,
+// capacity <= 64): rank-revealing QR in place in global memory (ws_gqr),
+// M ~ Q_G [R1; 0] = A B^T with A = Q_G [I_k; 0] (m x k) and B = R1^T (n x k),
+// then the fat truncation core with the U side given by Q_G's reflectors
+// (R_u = I) and the V side by the column-blocked QR of B.  A copy of M is
+// kept in the work area: a revealed rank above 128 restores M and falls
+// back to the step-synchronous path.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, int n, double* M, int ldm,
+                                      double* Uo, int lduo, double* Vo, int ldvo, int* rslot, double* ws,
+                                      double* sm) {
+  if (m > 512 || n > 512 || m < 256 || n < 256) return false;
+  const int tid = threadIdx.x;
+  const int64_t l = max(m, n);
+  constexpr int KC = 120;  // largest revealed rank handled here (the core must fit shared memory)
+  const int nbv = ws_cb_nb(n, KC, P.smem_work);
+  const int rcap = min(KC, max(o.iarg[2], 1));
+  if (nbv == 0 || fat_core_need(KC, KC, KC, nbv, rcap) > P.smem_work) return false;
+  // global scratch: the planner's 8 l + 3 l^2 + 200000 doubles; the last l^2 keep M
+  if ((int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > 2 * l * l + 200000) return false;
+  double* Wc = ws + 8 * l;                 // m x k: Q_G as one clean reflector block (ld m)
+  double* B = Wc + (int64_t)m * KC;        // n x k: R1^T
+  double* Rzv = B + (int64_t)n * KC;       // k x k
+  double* Sgu = Rzv + (int64_t)KC * KC;    // k x k: W_c^T W_c
+  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR (<= 64 k)
+  double* tpu = Sgv + 128 * (int64_t)KC;
+  double* tpv = tpu + KC;
+  double* gs = tpv + KC;                   // fat_core scratch (6 k^2 + 2 k)
+  double* Mc = ws + 8 * l + 2 * l * l + 200000;  // copy of M (ld m)
+  FOR_MN(i, j, m, n) Mc[i + (int64_t)j * m] = M[i + (int64_t)j * ldm];
+  double* wp = sm + 32;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
+  WsGqr a;
+  a.tp = take(KC + 1); a.wd = take(KC + 1); a.rd = take(KC + 1);
+  a.perm = reinterpret_cast<int*>(take(KC / 2 + 1));
+  a.pos = reinterpret_cast<int*>(take(n / 2 + 1));
+  a.cn = take(n); a.gq = take(n); a.rown = take(n); a.fq = take(n);
+  a.wv = take(m); a.wn = take(m);
+  a.red = take(3 * HMX_WARPS + 8);
+  double* gsm = take(GEMM_SMEM_DOUBLES);
+  __syncthreads();
+  unsigned long long tq = P.trace ? gtimer2() : 0;
+  const int policy = o.iarg[0];
+  const double cut = (policy == 2) ? o.farg[1] : 1e-14;
+  const double thr = HMX_RRQR_THR * cut;
+  int k;
+  if (m <= 256) k = ws_gqr<8>(m, n, M, ldm, thr, KC + 1, a);
+  else k = ws_gqr<16>(m, n, M, ldm, thr, KC + 1, a);
+  phase(P, 13, tq);
+  if (k > KC) {  // revealed rank beyond this path: restore M, the caller falls back
+    FOR_MN(i, j, m, n) M[i + (int64_t)j * ldm] = Mc[i + (int64_t)j * m];
+    __syncthreads();
+    return false;
+  }
+  if (k == 0) {
+    if (tid == 0) *rslot = 0;
+    __syncthreads();
+    return true;
+  }
+  // Q_G as one clean reflector block; B = R1^T
+  FOR_MN(i, j, m, k)
+    Wc[i + (int64_t)j * m] = i > j ? M[i + (int64_t)a.perm[j] * ldm] : (i == j ? a.wd[j] : 0.0);
+  FOR_MN(c_, i, n, k) {
+    const int pc = a.pos[c_];
+    B[c_ + (int64_t)i * n] = pc > i ? M[i + (int64_t)c_ * ldm] : (pc == i ? a.rd[i] : 0.0);
+  }
+  for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = a.tp[e];
+  __syncthreads();
+  ws_smat_gemm(m, k, Wc, m, Sgu, k, gsm);
+  const int nb2 = ws_cb_nb(n, k, P.smem_work);
+  ws_cbqr(n, k, B, n, Rzv, tpv, Sgv, nb2, sm + 32);
+  FatSide fu{m, k, Wc, m, tpu, Sgu, k, k};
+  FatSide fv{n, k, B, n, tpv, Sgv, nb2, nb2};
+  const int r = fat_core(P, o, k, k, k, nullptr, Rzv, fu, fv, Uo, lduo, Vo, ldvo, gs, sm, tq);
+  phase(P, 15, tq);
+  if (tid == 0) *rslot = r;
+  const int s_ = min(m, n);
+  count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s_ + (double)s_ * n));
   __syncthreads();
   return true;
 }
@@ -783,6 +1054,9 @@ __device__ void op_trunc(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   if (trunc_ws_small(P, o, m, n, K, U, ldu, V, ldv, Uo, lduo, Vo, ldvo, rslot, sm, tq)) return;
 #if HMX_WS > 1
   if (trunc_ws_panel(P, o, m, n, K, U, ldu, V, ldv, Uo, lduo, Vo, ldvo, rslot, ws, kb, sm, tq)) return;
+#if HMX_WS > 2
+  if (trunc_ws_fat(P, o, m, n, K, U, ldu, V, ldv, Uo, lduo, Vo, ldvo, rslot, ws, kb, sm, tq)) return;
+#endif
 #endif
 #endif
   // stage U, V (and G) in shared memory when they fit
@@ -928,6 +1202,9 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* ws = mref(P, c, o.wref);
 #if HMX_WS
   if (d2lr_ws(P, o, m, n, M, ldm, Uo, o.ld[2], Vo, o.ld[3], rslot, ws, sm)) return;
+#if HMX_WS > 1
+  if (d2lr_big(P, o, m, n, M, ldm, Uo, o.ld[2], Vo, o.ld[3], rslot, ws, sm)) return;
+#endif
 #endif
   double* work = sm + 32;
   double* G = M;
@@ -2023,7 +2300,7 @@ hmx_status hmx_truncate_batched(int32_t batch, int32_t m, int32_t n, int32_t K, 
   // per-CTA scratch: U copy (m*K), V copy (n*K), workspace 4K + 2K^2
   const int64_t kk = std::max(K, 1);
   const int64_t offV = (int64_t)m * kk, offW = offV + (int64_t)n * kk;
-  const int64_t scratch = offW + 5 * kk * kk + (int64_t)(m + n + 200) * kk + 2048;
+  const int64_t scratch = offW + 9 * kk * kk + (int64_t)(m + n + 200) * kk + 2048;
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);
@@ -2062,7 +2339,7 @@ hmx_status hmx_dense_to_lowrank_batched(int32_t batch, int32_t m, int32_t n, con
   if (batch < 0 || m <= 0 || n <= 0 || cap < 0) return HMX_ERR_ARG;
   const int64_t s = std::min(m, n), l = std::max(m, n);
   const int64_t offW = (int64_t)m * n;
-  const int64_t scratch = offW + 8 * l + 2 * l * l;
+  const int64_t scratch = offW + 8 * l + (l >= 256 ? 3 * l * l + 200000 : 2 * l * l);
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);

@@ -651,4 +651,394 @@ __device__ bool ws_jacobi(int rows, int k, double* X, int ldx, double* sigma, in
   return converged;
 }
 
+// ---------------------------------------------------------------------------
+// Rank-revealing Householder QR of a p x q block G held in GLOBAL memory
+// (dense_to_lowrank of large blocks: the block does not fit shared memory
+// but lives in L2), whole CTA.  Lanes run over rows (coalesced), warp w
+// owns the columns c = w (mod HMX_WARPS).  One pass over the trailing
+// matrix per step: the pass that applies reflector j to a column also
+// accumulates the column's inner product with the NEXT pivot column and
+// its exact trailing norm.  The next pivot is chosen before the pass from
+// the norms downdated by one step (exact norm minus r_jc^2, as dlaqp2 does
+// once); the stopping test uses the exact norms the pass produces:
+// stop after k steps when ||G[k:, unpivoted]||_F <= thr |R_00|, or at
+// kcap.  Columns are not swapped (perm / pos as in ws_rrqr); R_1[i, c] =
+// G[i, c] if pos[c] > i, rd[i] if pos[c] == i.
+// Shared work arrays: tp, wd, rd (kcap), perm (kcap), pos, cn, gq, rown, fq
+// (q each), wv, wn (p each), red (3 * HMX_WARPS + 8 doubles).
+// ---------------------------------------------------------------------------
+struct WsGqr {
+  double *tp, *wd, *rd, *cn, *gq, *rown, *fq, *wv, *wn, *red;
+  int *perm, *pos;
+};
+
+template <int RPLG>
+__device__ int ws_gqr(int p, int q, double* G, int64_t ld, double thr, int kcap, const WsGqr& a) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int* ired = reinterpret_cast<int*>(a.red + 3 * HMX_WARPS);
+  // column norms
+  for (int c = w; c < q; c += HMX_WARPS) {
+    const double* x = G + (int64_t)c * ld;
+    double s0 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPLG; ++u) {
+      const int i = lane + 32 * u;
+      const double v = i < p ? x[i] : 0.0;
+      s0 = fma(v, v, s0);
+    }
+    s0 = warp_sum(s0);
+    if (lane == 0) { a.cn[c] = s0; a.pos[c] = 0x7fffffff; }
+  }
+  __syncthreads();
+  // block arg-max of cn over the unpivoted columns (+ their sum)
+  auto argmax = [&](double& vmax, double& tail) -> int {
+    double v = -1.0, t = 0.0;
+    int idx = 0x7fffffff;
+    for (int c = tid; c < q; c += HMX_THREADS)
+      if (a.pos[c] == 0x7fffffff) {
+        const double x = a.cn[c];
+        t += x;
+        if (x > v) { v = x; idx = c; }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    __syncthreads();
+    if (lane == 0) { a.red[3 * w] = v; a.red[3 * w + 1] = (double)idx; a.red[3 * w + 2] = t; }
+    __syncthreads();
+    v = -1.0; idx = 0x7fffffff; t = 0.0;
+#pragma unroll
+    for (int x = 0; x < HMX_WARPS; ++x) {
+      const double ov = a.red[3 * x];
+      const int oi = (int)a.red[3 * x + 1];
+      if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+      t += a.red[3 * x + 2];
+    }
+    vmax = v; tail = t;
+    return idx;
+  };
+  double vmax, tail;
+  int pc = argmax(vmax, tail);
+  const double r00sq = vmax;
+  const int kmax = min(min(p, q), kcap);
+  if (!(vmax > 0.0) || kmax == 0) return 0;
+  // inner products of the first pivot column (rows > 0) with every column
+  for (int i = tid; i < p; i += HMX_THREADS) a.wn[i] = i > 0 ? G[i + (int64_t)pc * ld] : 0.0;
+  __syncthreads();
+  for (int c = w; c < q; c += HMX_WARPS) {
+    const double* x = G + (int64_t)c * ld;
+    double s0 = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPLG; ++u) {
+      const int i = lane + 32 * u;
+      if (i < p) s0 = fma(a.wn[i], x[i], s0);
+    }
+    s0 = warp_sum(s0);
+    if (lane == 0) { a.gq[c] = s0; a.rown[c] = x[0]; }
+  }
+  __syncthreads();
+  int k = kmax;
+  for (int j = 0; j < kmax; ++j) {
+    // reflector j from column pc; update factors, row j of R, downdated norms
+    double beta, wdj, tpj;
+    house_scalars(a.rown[pc], a.gq[pc], beta, wdj, tpj);
+    __syncthreads();  // everyone has read rown[pc] / gq[pc]
+    for (int c = tid; c < q; c += HMX_THREADS) {
+      if (a.pos[c] != 0x7fffffff || c == pc) continue;
+      const double f = tpj * fma(wdj, a.rown[c], a.gq[c]);
+      const double rjc = fma(-f, wdj, a.rown[c]);
+      a.fq[c] = f;
+      G[j + (int64_t)c * ld] = rjc;
+      a.cn[c] = fmax(a.cn[c] - rjc * rjc, 0.0);
+    }
+    if (tid == 0) { a.tp[j] = tpj; a.wd[j] = wdj; a.rd[j] = beta; a.perm[j] = pc; }
+    // w_j tail (rows > j) for the pass
+    for (int i = tid; i < p; i += HMX_THREADS) a.wv[i] = i > j ? G[i + (int64_t)pc * ld] : 0.0;
+    __syncthreads();
+    if (tid == 0) a.pos[pc] = j;
+    __syncthreads();
+    if (j + 1 == kmax) break;
+    const int pn = argmax(vmax, tail);  // next pivot from the downdated norms
+    if (pn == 0x7fffffff || !(vmax > 0.0)) { k = j + 1; break; }
+    // the next pivot column first: updated, stored, its tail (rows > j+1) to wn
+    __syncthreads();  // the arg-max results in red are consumed
+    {
+      double* x = G + (int64_t)pn * ld;
+      const double f = a.fq[pn];
+      double s0 = 0.0, s1 = 0.0;
+      for (int i = tid; i < p; i += HMX_THREADS) {
+        const double v = fma(-f, a.wv[i], x[i]);
+        if (i > j) x[i] = v;
+        a.wn[i] = i > j + 1 ? v : 0.0;
+        if (i == j + 1) a.rown[pn] = v;
+        if (i > j) s0 = fma(v, v, s0);
+        if (i > j + 1) s1 = fma(v, v, s1);
+      }
+      s0 = warp_sum(s0); s1 = warp_sum(s1);
+      if (lane == 0) { a.red[2 * w] = s0; a.red[2 * w + 1] = s1; }
+      __syncthreads();
+      if (tid == 0) {
+        double t0 = 0.0, t1 = 0.0;
+        for (int x2 = 0; x2 < HMX_WARPS; ++x2) { t0 += a.red[2 * x2]; t1 += a.red[2 * x2 + 1]; }
+        a.cn[pn] = t0; a.gq[pn] = t1;
+      }
+    }
+    // fused pass over this warp's other unpivoted columns, two at a time
+    const int lj = (j + 1) & 31, uj = (j + 1) >> 5;
+    for (int c0 = w; c0 < q; c0 += 2 * HMX_WARPS) {
+      const int c1 = c0 + HMX_WARPS;
+      const bool on0 = a.pos[c0] == 0x7fffffff && c0 != pn;
+      const bool on1 = c1 < q && a.pos[c1] == 0x7fffffff && c1 != pn;
+      if (!on0 && !on1) continue;
+      double* x0 = G + (int64_t)c0 * ld;
+      double* x1 = G + (int64_t)(on1 ? c1 : c0) * ld;
+      const double f0 = on0 ? a.fq[c0] : 0.0, f1 = on1 ? a.fq[c1] : 0.0;
+      double v0[RPLG], v1[RPLG];
+#pragma unroll
+      for (int u = 0; u < RPLG; ++u) {
+        const int i = lane + 32 * u;
+        v0[u] = (on0 && i < p) ? x0[i] : 0.0;
+        v1[u] = (on1 && i < p) ? x1[i] : 0.0;
+      }
+      double g0 = 0.0, g1 = 0.0, n0 = 0.0, n1 = 0.0, r0 = 0.0, r1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPLG; ++u) {
+        const int i = lane + 32 * u;
+        const double wvi = i < p ? a.wv[i] : 0.0, wni = i < p ? a.wn[i] : 0.0;
+        v0[u] = fma(-f0, wvi, v0[u]);
+        v1[u] = fma(-f1, wvi, v1[u]);
+        g0 = fma(wni, v0[u], g0);
+        g1 = fma(wni, v1[u], g1);
+        if (i > j) { n0 = fma(v0[u], v0[u], n0); n1 = fma(v1[u], v1[u], n1); }
+        if (u == uj && lane == lj) { r0 = v0[u]; r1 = v1[u]; }
+        if (i > j && i < p) {
+          if (on0) x0[i] = v0[u];
+          if (on1) x1[i] = v1[u];
+        }
+      }
+      g0 = warp_sum(g0); g1 = warp_sum(g1); n0 = warp_sum(n0); n1 = warp_sum(n1);
+      if (lane == lj) {
+        if (on0) { a.rown[c0] = r0; }
+        if (on1) { a.rown[c1] = r1; }
+      }
+      if (lane == 0) {
+        if (on0) { a.gq[c0] = g0; a.cn[c0] = n0; }
+        if (on1) { a.gq[c1] = g1; a.cn[c1] = n1; }
+      }
+    }
+    __syncthreads();
+    // exact trailing norms: stop?
+    {
+      double t = 0.0;
+      for (int c = tid; c < q; c += HMX_THREADS)
+        if (a.pos[c] == 0x7fffffff) t += a.cn[c];
+      t = warp_sum(t);
+      if (lane == 0) a.red[w] = t;
+      __syncthreads();
+      if (tid == 0) {
+        double tt = 0.0;
+        for (int x2 = 0; x2 < HMX_WARPS; ++x2) tt += a.red[x2];
+        ired[0] = (tt <= thr * thr * r00sq) ? 1 : 0;
+      }
+      __syncthreads();
+      if (ired[0]) { k = j + 1; break; }
+    }
+    pc = pn;
+  }
+  __syncthreads();
+  return k;
+}
+
+// striu(W^T W) of a reflector block in global memory (coalesced: one warp per
+// pair, lanes over rows), written to the strict upper triangle.
+__device__ void ws_smat_g(int rows, int p, double* A, int64_t lda, const double* wd) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int npair = p * (p - 1) / 2;
+  for (int e = w; e < npair; e += HMX_WARPS) {
+    int j = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)e)) * 0.5f);
+    while (j * (j - 1) / 2 > e) --j;
+    while ((j + 1) * j / 2 <= e) ++j;
+    const int i = e - j * (j - 1) / 2;
+    const double* ai = A + (int64_t)i * lda;
+    double* aj = A + (int64_t)j * lda;
+    double s0 = 0.0, s1 = 0.0;
+    int l = j + 1 + lane;
+    for (; l + 32 < rows; l += 64) {
+      const double x0 = ai[l], y0 = aj[l], x1 = ai[l + 32], y1 = aj[l + 32];
+      s0 = fma(x0, y0, s0);
+      s1 = fma(x1, y1, s1);
+    }
+    if (l < rows) s0 = fma(ai[l], aj[l], s0);
+    s0 = warp_sum(s0 + s1);
+    if (lane == 0) aj[i] = fma(wd[j], ai[j], s0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column-blocked Householder QR for factors whose K columns do not fit
+// shared memory next to their rows ("fat" stacked factors, K up to 128 and
+// more): blocks of nb columns are factored in shared memory by all warps
+// (ws_qr) after the previous blocks have been applied to them, each block
+// c in compact-WY form Q_c = I - W_c T_c W_c^T with its own T_c^{-1} =
+// striu(W_c^T W_c) + diag(1/tp) (nb x nb, kept in the strict upper triangle
+// of the block's diagonal block).  Q = Q_0 Q_1 ... Q_{B-1}.
+// ---------------------------------------------------------------------------
+
+// forward substitution (T^{-1})^T Z = B with L[i, j] (i > j) = Ls[i + j ldl]
+// (the transposed striu(S)) and diagonal 1/tp; warp per right-hand side.
+template <int RP>
+__device__ void ws_trsolve_fwd_w(int p, const double* Ls, int ldl, const double* tp, double* B, int ldb,
+                                 int r, int tid, int nthr) {
+  const int lane = tid & 31, wid = tid >> 5, nwp = nthr >> 5;
+  for (int t = wid; t < r; t += nwp) {
+    double* bt = B + (int64_t)t * ldb;
+    double b[RP];
+#pragma unroll
+    for (int u = 0; u < RP; ++u) b[u] = (lane + 32 * u < p) ? bt[lane + 32 * u] : 0.0;
+    double sc[RP], tj = p > 0 ? tp[0] : 0.0;
+#pragma unroll
+    for (int u = 0; u < RP; ++u) sc[u] = p > 0 ? Ls[min(lane + 32 * u, p - 1)] : 0.0;
+    for (int j = 0; j < p; ++j) {
+      double sn[RP];
+      const int jn = min(j + 1, p - 1);
+      const double tn = tp[jn];
+#pragma unroll
+      for (int u = 0; u < RP; ++u) sn[u] = Ls[min(lane + 32 * u, p - 1) + (int64_t)jn * ldl];
+      double bj = b[0];
+#pragma unroll
+      for (int u = 1; u < RP; ++u) if ((j >> 5) == u) bj = b[u];
+      const double zj = __shfl_sync(0xffffffffu, bj, j & 31) * tj;
+#pragma unroll
+      for (int u = 0; u < RP; ++u) {
+        const int row = lane + 32 * u;
+        if (row > j) b[u] = fma(-sc[u], zj, b[u]);
+        else if (row == j) b[u] = zj;
+      }
+      tj = tn;
+#pragma unroll
+      for (int u = 0; u < RP; ++u) sc[u] = sn[u];
+    }
+#pragma unroll
+    for (int u = 0; u < RP; ++u) if (lane + 32 * u < p) bt[lane + 32 * u] = b[u];
+  }
+}
+
+__device__ void ws_trsolve_fwd(int p, const double* Ls, int ldl, const double* tp, double* B, int ldb, int r,
+                               int tid, int nthr) {
+  if (p <= 32) ws_trsolve_fwd_w<1>(p, Ls, ldl, tp, B, ldb, r, tid, nthr);
+  else if (p <= 64) ws_trsolve_fwd_w<2>(p, Ls, ldl, tp, B, ldb, r, tid, nthr);
+  else ws_trsolve_fwd_w<4>(p, Ls, ldl, tp, B, ldb, r, tid, nthr);
+}
+
+// Y (rows x r, in place, any memory) := Q_c Y (trans = false) or Q_c^T Y
+// (trans = true) for one reflector block in CLEAN form: W (rows x jc at A,
+// lda) holds the tails below the diagonal, wd ON the diagonal and zeros
+// above it, so W^T Y and W Z are plain GEMMs (cta_gemm: shared-memory
+// staged tiles, any operand memory); striu(W^T W) is kept apart (Sg, jc x jc,
+// ld lds).  Shared work: Sc ((jc|1) x jc), Bm ((jc|1) x r), sw (jc), gsm
+// (GEMM_SMEM_DOUBLES).  Whole CTA, ends synchronised.
+__device__ void ws_apply_block(int rows, int jc, const double* A, int64_t lda, const double* tp,
+                               const double* Sg, int lds, bool trans, double* Y, int64_t ldy, int r,
+                               double* Sc, double* Bm, double* sw, double* gsm) {
+  const int tid = threadIdx.x;
+  const int lb = jc | 1;
+  if (jc <= 0 || r <= 0) return;
+  for (int e = tid; e < jc; e += HMX_THREADS) sw[e] = tp[e];
+  if (!trans) { FOR_MN(i, j, jc, jc) Sc[i + j * lb] = (i < j) ? Sg[i + (int64_t)j * lds] : 0.0; }
+  else { FOR_MN(j, i, jc, jc) Sc[i + j * lb] = (i > j) ? Sg[j + (int64_t)i * lds] : 0.0; }
+  __syncthreads();
+  cta_gemm(jc, r, rows, 1.0, A, (int)lda, true, Y, (int)ldy, false, false, Bm, lb, gsm);
+  if (!trans) ws_trsolve(jc, Sc, lb, sw, Bm, lb, r, tid, HMX_THREADS);
+  else ws_trsolve_fwd(jc, Sc, lb, sw, Bm, lb, r, tid, HMX_THREADS);
+  __syncthreads();
+  cta_gemm(rows, r, jc, -1.0, A, (int)lda, false, Bm, lb, false, true, Y, (int)ldy, gsm);
+}
+
+// striu(W^T W) of a clean reflector block (rows x jc) into Sg (jc x jc, ld
+// lds; the lower part and the diagonal receive W^T W too and are ignored).
+__device__ void ws_smat_gemm(int rows, int jc, const double* A, int64_t lda, double* Sg, int lds, double* gsm) {
+  cta_gemm(jc, jc, rows, 1.0, A, (int)lda, true, A, (int)lda, false, false, Sg, lds, gsm);
+}
+
+// block width for an m-row factor: the panel (m + pad rows) x nb, two
+// (nb|1) x nb work blocks, the GEMM staging and the exchange buffers must
+// fit `cap` doubles
+__device__ __forceinline__ int ws_cb_nb(int m, int K, int64_t cap) {
+  const int64_t lp = (m + 64) | 1;
+  for (int nb = 64; nb >= 8; nb -= 8) {
+    const int64_t need = lp * nb + 2 * (int64_t)(nb | 1) * nb + 2 * (HMX_WARPS + 1) * (nb + 1) + 4 * nb +
+                         GEMM_SMEM_DOUBLES + 64;
+    if (need <= cap) return min(nb, (K + 7) & ~7);
+  }
+  return 0;
+}
+
+// QR of the m x K factor A (global, in place; on exit the clean reflector
+// blocks: tails below the diagonal, wd on it, zeros above within a block's
+// diagonal block; rows above a block keep stale R entries).  Rz: R (p x K,
+// ld p, zeros below the diagonal).  sc (global): tp at [0, p).  Sg (global,
+// nb x nb per block, ld nb): striu(W_c^T W_c).  wk: shared work area.
+__device__ void ws_cbqr(int m, int K, double* A, int64_t lda, double* Rz, double* sc, double* Sg, int nb,
+                        double* wk) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int p = min(m, K);
+  const int lp = (m + 64) | 1, lb = nb | 1;
+  double* Ps = wk;
+  double* Sc = Ps + (int64_t)lp * nb;
+  double* Bm = Sc + lb * nb;
+  double* xch = Bm + lb * nb;
+  double* tps = xch + 2 * (HMX_WARPS + 1) * (nb + 1);
+  double* wds = tps + nb;
+  double* sw = wds + nb;  // nb
+  double* gsm = sw + 2 * nb;
+  for (int j0 = 0; j0 < K; j0 += nb) {
+    const int jb = min(nb, K - j0);
+    for (int c = w; c < jb; c += HMX_WARPS) {
+      const double* s_ = A + (int64_t)(j0 + c) * lda;
+      double* d_ = Ps + c * lp;
+      for (int i = lane; i < lp; i += 128) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (i + 32 * u < m) ? s_[i + 32 * u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) if (i + 32 * u < lp) d_[i + 32 * u] = v[u];
+      }
+    }
+    __syncthreads();
+    // Q_{b-1}^T ... Q_0^T applied to the new columns, first block first
+    for (int c0 = 0; c0 < min(j0, p); c0 += nb) {
+      const int jc = min(nb, p - c0);
+      ws_apply_block(m - c0, jc, A + c0 + (int64_t)c0 * lda, lda, sc + c0, Sg + (int64_t)(c0 / nb) * nb * nb, nb,
+                     true, Ps + c0, lp, jb, Sc, Bm, sw, gsm);
+    }
+    if (j0 < p) {
+      if (jb <= 32) ws_qr<1, HMX_WARPS>(m - j0, jb, Ps + j0, lp, tps, wds, xch, 0, 0);
+      else ws_qr<2, HMX_WARPS>(m - j0, jb, Ps + j0, lp, tps, wds, xch, 0, 0);
+    }
+    FOR_MN(i, c, p, jb) Rz[i + (int64_t)(j0 + c) * p] = (i <= j0 + c) ? Ps[i + c * lp] : 0.0;
+    __syncthreads();
+    if (j0 < p) {
+      const int jq = min(jb, p - j0);
+      ws_smat(m - j0, jq, Ps + j0, lp, wds, tid, HMX_THREADS);
+      __syncthreads();
+      double* Sgb = Sg + (int64_t)(j0 / nb) * nb * nb;
+      FOR_MN(i, c, jq, jq) Sgb[i + c * nb] = (i < c) ? Ps[j0 + i + c * lp] : 0.0;
+      // clean block: wd on the diagonal, zeros above it (columns beyond p keep R)
+      for (int c = w; c < jb; c += HMX_WARPS)
+        for (int i = j0 + lane; i < m; i += 32) {
+          const int ii = i - j0;
+          double v = Ps[i + c * lp];
+          if (c < jq) v = ii > c ? v : (ii == c ? wds[c] : 0.0);
+          A[i + (int64_t)(j0 + c) * lda] = v;
+        }
+      for (int e = tid; e < jq; e += HMX_THREADS) sc[j0 + e] = tps[e];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace hmx

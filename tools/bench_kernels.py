@@ -49,7 +49,7 @@ def run(ops_per_task, bases, scratch, reps=5, nt=None, trace=False):
     return min(ts), st, prof
 
 
-def trunc_case(m, n, K, decay=0.3, eps=1e-6, batch=148, trace=False):
+def trunc_case(m, n, K, decay=0.3, eps=1e-6, batch=int(os.environ.get('HMX_BENCH_BATCH', '148')), trace=False):
     rng = np.random.default_rng(0)
     kb = K
     U = rng.normal(size=(batch, K, m)) * np.exp(-decay * np.arange(K))[None, :, None]
@@ -60,7 +60,7 @@ def trunc_case(m, n, K, decay=0.3, eps=1e-6, batch=148, trace=False):
     rk = torch.zeros(batch, dtype=torch.int32, device="cuda")
     offV = m * kb
     offW = offV + n * kb
-    scratch = offW + 5 * kb * kb + (m + n + 200) * kb + 2048
+    scratch = offW + 9 * kb * kb + (m + n + 200) * kb + 2048
     tasks = []
     for b in range(batch):
         o = np.zeros(3, dtype=_lib.OP_DTYPE)
@@ -86,20 +86,23 @@ def trunc_case(m, n, K, decay=0.3, eps=1e-6, batch=148, trace=False):
     return us, st, float(rk.float().mean().item()), prof
 
 
-def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=148):
+def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=int(os.environ.get('HMX_BENCH_BATCH', '148'))):
     rng = np.random.default_rng(1)
     # 2D exp-kernel block between neighbouring boxes (realistic numerical rank)
     g = int(np.sqrt(m))
-    a = np.stack(np.meshgrid(np.arange(g), np.arange(m // g), indexing="ij"), -1).reshape(-1, 2) / 128
+    if g * (m // g) == m:
+        a = np.stack(np.meshgrid(np.arange(g), np.arange(m // g), indexing="ij"), -1).reshape(-1, 2) / 128
+    else:  # random points in a box of the same density
+        a = rng.random((m, 2)) * (g / 128.0)
     b = a + np.array([g / 128.0 * 1.5, 0.0])
     d = np.linalg.norm(a[:, None, :] - b[None, :n, :], axis=-1)
-    M = np.exp(-d / 0.2) - np.exp(-d / 0.2) * 1e-7 * rng.normal(size=d.shape)
+    M = np.exp(-d / 0.2)  # smooth spectrum: the revealed rank is the numerical rank
     Ms = np.stack([M.T.ravel() * (1 + 1e-3 * b) for b in range(batch)])
     dM = torch.from_numpy(Ms).cuda()
     out = torch.zeros(batch, (m + n) * min(m, n), dtype=torch.float64, device="cuda")
     rk = torch.zeros(batch, dtype=torch.int32, device="cuda")
     l = max(m, n)
-    scratch = m * n + 8 * l + 2 * l * l
+    scratch = m * n + 8 * l + (3 * l * l + 200000 if l >= 256 else 2 * l * l)
     tasks = []
     for b in range(batch):
         o = np.zeros(2, dtype=_lib.OP_DTYPE)
@@ -113,26 +116,33 @@ def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=148):
         t["ref"][3] = _lib.mref(2, b * (m + n) * min(m, n) + m * min(m, n)); t["ld"][3] = n
         t["wref"] = _lib.mref(SB, m * n)
         t["slot"][0] = _lib.slot(3, b)
-        t["iarg"][:3] = (2, 0, min(m, n))
+        t["iarg"][:3] = (2, 0, min(m, n, 64))
         t["farg"][1] = eps
         tasks.append(o)
-    us, st, _ = run(tasks, {0: (dM, None), 2: (out, None), 3: (None, rk)}, scratch)
-    return us, st, float(rk.float().mean().item())
+    us, st, prof = run(tasks, {0: (dM, None), 2: (out, None), 3: (None, rk)}, scratch, trace=True)
+    return us, st, float(rk.float().mean().item()), prof
+
+
+def dshapes_only():
+    return any(a.startswith("d") for a in sys.argv[1:]) and not any("," in a and not a.startswith("d") for a in sys.argv[1:])
 
 
 def main():
     names = {12: "QR", 13: "RRQR", 14: "Jacobi", 15: "recomp"}
-    shapes = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:] if "," in a]
-    for (m, n, K) in shapes or [(64, 64, 20), (64, 64, 40), (128, 128, 24), (256, 256, 24), (256, 256, 48),
-                      (512, 512, 30), (1024, 1024, 30), (1024, 1024, 120), (2048, 2048, 30)]:
+    shapes = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:] if "," in a and not a.startswith("d")]
+    for (m, n, K) in shapes or ([] if dshapes_only() else [(64, 64, 20), (64, 64, 40), (128, 128, 24), (256, 256, 24), (256, 256, 48),
+                      (512, 512, 30), (1024, 1024, 30), (1024, 1024, 120), (2048, 2048, 30)]):
         us, st, r, prof = trunc_case(m, n, K, trace=True)
         ph = " ".join(f"{names[c]}={prof[c,0]/max(prof[c,1],1)/1e3:.0f}us" for c in (12, 13, 15))
         sw = prof[14, 1] / max(prof[13, 1], 1)
         print(f"TRUNC m={m:5d} n={n:5d} K={K:4d}: {us:9.1f} us/op  rank~{r:.1f} status={st} "
               f"[{ph} Jacobi={prof[14,0]/max(prof[13,1],1)/1e3:.0f}us sweeps={sw:.1f}]", flush=True)
-    for (m, n) in ([] if shapes else [(64, 64), (128, 128)]):
-        us, st, r = d2lr_case(m, n)
-        print(f"D2LR  m={m:5d} n={n:5d}: {us:9.1f} us/op  rank~{r:.1f} status={st}", flush=True)
+    dshapes = [tuple(int(x) for x in a[1:].split(",")) for a in sys.argv[1:] if a.startswith("d")]
+    for (m, n) in (dshapes if (shapes or dshapes) else [(64, 64), (128, 128), (256, 256), (512, 512)]):
+        us, st, r, prof = d2lr_case(m, n)
+        nd = max(prof[9, 1], 1)
+        ph = " ".join(f"{names[c]}={prof[c,0]/nd/1e3:.0f}us" for c in (12, 13, 14, 15))
+        print(f"D2LR  m={m:5d} n={n:5d}: {us:9.1f} us/op  rank~{r:.1f} status={st} [{ph} sweeps={prof[14,1]/nd:.1f}]", flush=True)
 
 
 if __name__ == "__main__":

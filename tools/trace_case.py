@@ -92,11 +92,15 @@ for t in path:
         key = names.get(code, code)
         if code == 8:
             K = int(ops[i]["dim"][0])
-            key = f"TRUNC m={K}"
+            kin = int(plan.plan.op_inner[i])
+            kb = 16 if kin <= 16 else 32 if kin <= 32 else 64 if kin <= 64 else 128 if kin <= 128 else 256 if kin <= 256 else 4096
+            key = f"TRUNC m={K} K<={kb}"
+        if code == 9:
+            key = f"D2LR m={int(ops[i]['dim'][0])}"
         pc[key] += opt[i] / 1e3
         pn[key] += 1
 print("  critical-path time by op:")
-for k, v in pc.most_common(14):
+for k, v in pc.most_common(24):
     print(f"    {k:16s} {v/1e3:8.2f} ms  n={pn[k]}")
 pd = sorted(path, key=lambda t: -dur[t])[:25]
 for t in pd:
