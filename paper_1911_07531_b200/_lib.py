@@ -187,7 +187,7 @@ class Plan:
         if task_scratch is not None and len(task_scratch):
             ts = np.ascontiguousarray(task_scratch, dtype=np.int64)
             peak = int(ts.max())
-            small = max(int(np.percentile(ts, 99.9)), 1 << 16)
+            small = max(int(np.percentile(ts, float(os.environ.get("HMX_SCRATCH_PCT", "99.9")))), 1 << 16)
             if scratch_budget:
                 nct = (max_ctas or 148 * max(1, int(ctas_per_sm)))
                 small = min(small, max(1 << 16, int(scratch_budget) // 2 // 8 // nct))

@@ -942,49 +942,82 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
 __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, int n, double* M, int ldm,
                                       double* Uo, int lduo, double* Vo, int ldvo, int* rslot, double* ws,
                                       double* sm) {
-  if (m > 512 || n > 512 || m < 256 || n < 256) return false;
+  const bool mid = m <= 128 && n <= 128;  // pivoted QR in shared memory (M stays intact)
+  if (!mid && (m > 512 || n > 512 || m < 256 || n < 256)) return false;
+  if (mid && (m < 16 || n < 16)) return false;
   const int tid = threadIdx.x;
   const int64_t l = max(m, n);
-  constexpr int KC = 120;  // largest revealed rank handled here (the core must fit shared memory)
+  const int KC = mid ? min(m, n) : 120;  // largest revealed rank handled here (the core must fit shared memory)
   const int nbv = ws_cb_nb(n, KC, P.smem_work);
   const int rcap = min(KC, max(o.iarg[2], 1));
   if (nbv == 0 || fat_core_need(KC, KC, KC, nbv, rcap) > P.smem_work) return false;
-  // global scratch: the planner's 8 l + 3 l^2 + 200000 doubles; the last l^2 keep M
-  if ((int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > 2 * l * l + 200000) return false;
+  // global scratch (planner): 8 l + 16 l^2 (l < 256) or 8 l + 3 l^2 + 200000, the last l^2 keep M
+  const int64_t avail = mid ? 16 * l * l : 2 * l * l + 200000;
+  if ((int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > avail) return false;
   double* Wc = ws + 8 * l;                 // m x k: Q_G as one clean reflector block (ld m)
   double* B = Wc + (int64_t)m * KC;        // n x k: R1^T
   double* Rzv = B + (int64_t)n * KC;       // k x k
   double* Sgu = Rzv + (int64_t)KC * KC;    // k x k: W_c^T W_c
-  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR (<= 64 k)
+  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR
   double* tpu = Sgv + 128 * (int64_t)KC;
   double* tpv = tpu + KC;
   double* gs = tpv + KC;                   // fat_core scratch (6 k^2 + 2 k)
-  double* Mc = ws + 8 * l + 2 * l * l + 200000;  // copy of M (ld m)
-  FOR_MN(i, j, m, n) Mc[i + (int64_t)j * m] = M[i + (int64_t)j * ldm];
-  double* wp = sm + 32;
-  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
-  WsGqr a;
-  a.tp = take(KC + 1); a.wd = take(KC + 1); a.rd = take(KC + 1);
-  a.perm = reinterpret_cast<int*>(take(KC / 2 + 1));
-  a.pos = reinterpret_cast<int*>(take(n / 2 + 1));
-  a.cn = take(n); a.gq = take(n); a.rown = take(n); a.fq = take(n);
-  a.wv = take(m); a.wn = take(m);
-  a.red = take(3 * HMX_WARPS + 8);
-  double* gsm = take(GEMM_SMEM_DOUBLES);
-  __syncthreads();
   unsigned long long tq = P.trace ? gtimer2() : 0;
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
   const double thr = HMX_RRQR_THR * cut;
+  double* wp = sm + 32;
+  auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
   int k;
-  if (m <= 256) k = ws_gqr<8>(m, n, M, ldm, thr, KC + 1, a);
-  else k = ws_gqr<16>(m, n, M, ldm, thr, KC + 1, a);
-  phase(P, 13, tq);
-  if (k > KC) {  // revealed rank beyond this path: restore M, the caller falls back
-    FOR_MN(i, j, m, n) M[i + (int64_t)j * ldm] = Mc[i + (int64_t)j * m];
+  double *tpa, *wda, *rda;
+  int *perma, *posa;
+  const double* Gs;  // where the factored block lives
+  int64_t ldgs;
+  double* gsm;
+  if (mid) {
+    int* ired = reinterpret_cast<int*>(sm + 16);
+    tpa = take(n); wda = take(n); rda = take(n);
+    perma = reinterpret_cast<int*>(take(n));
+    posa = perma + n;
+    double* xr = take(32);
+    gsm = take(GEMM_SMEM_DOUBLES);
+    const int lg = m | 1;
+    double* G = take((int64_t)lg * n);
+    FOR_MN(i, j, m, n) G[i + j * lg] = M[i + (int64_t)j * ldm];
     __syncthreads();
-    return false;
+    const int nwr = (n + 31) >> 5;
+    if ((tid >> 5) < nwr) {
+      const int kk = ws_rrqr(m, n, G, lg, tpa, wda, rda, perma, posa, thr, xr, 0, nwr, 3);
+      if (tid == 0) ired[0] = kk;
+    }
+    __syncthreads();
+    k = ired[0];
+    Gs = G;
+    ldgs = lg;
+  } else {
+    double* Mc = ws + 8 * l + 2 * l * l + 200000;  // copy of M (ld m)
+    FOR_MN(i, j, m, n) Mc[i + (int64_t)j * m] = M[i + (int64_t)j * ldm];
+    WsGqr a;
+    a.tp = take(KC + 1); a.wd = take(KC + 1); a.rd = take(KC + 1);
+    a.perm = reinterpret_cast<int*>(take(KC / 2 + 1));
+    a.pos = reinterpret_cast<int*>(take(n / 2 + 1));
+    a.cn = take(n); a.gq = take(n); a.rown = take(n); a.fq = take(n);
+    a.wv = take(m); a.wn = take(m);
+    a.red = take(3 * HMX_WARPS + 8);
+    gsm = take(GEMM_SMEM_DOUBLES);
+    __syncthreads();
+    if (m <= 256) k = ws_gqr<8>(m, n, M, ldm, thr, KC + 1, a);
+    else k = ws_gqr<16>(m, n, M, ldm, thr, KC + 1, a);
+    if (k > KC) {  // revealed rank beyond this path: restore M, the caller falls back
+      FOR_MN(i, j, m, n) M[i + (int64_t)j * ldm] = Mc[i + (int64_t)j * m];
+      __syncthreads();
+      return false;
+    }
+    tpa = a.tp; wda = a.wd; rda = a.rd; perma = a.perm; posa = a.pos;
+    Gs = M;
+    ldgs = ldm;
   }
+  phase(P, 13, tq);
   if (k == 0) {
     if (tid == 0) *rslot = 0;
     __syncthreads();
@@ -992,12 +1025,12 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
   }
   // Q_G as one clean reflector block; B = R1^T
   FOR_MN(i, j, m, k)
-    Wc[i + (int64_t)j * m] = i > j ? M[i + (int64_t)a.perm[j] * ldm] : (i == j ? a.wd[j] : 0.0);
+    Wc[i + (int64_t)j * m] = i > j ? Gs[i + (int64_t)perma[j] * ldgs] : (i == j ? wda[j] : 0.0);
   FOR_MN(c_, i, n, k) {
-    const int pc = a.pos[c_];
-    B[c_ + (int64_t)i * n] = pc > i ? M[i + (int64_t)c_ * ldm] : (pc == i ? a.rd[i] : 0.0);
+    const int pc = posa[c_];
+    B[c_ + (int64_t)i * n] = pc > i ? Gs[i + (int64_t)c_ * ldgs] : (pc == i ? rda[i] : 0.0);
   }
-  for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = a.tp[e];
+  for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = tpa[e];
   __syncthreads();
   ws_smat_gemm(m, k, Wc, m, Sgu, k, gsm);
   const int nb2 = ws_cb_nb(n, k, P.smem_work);
@@ -2339,7 +2372,7 @@ hmx_status hmx_dense_to_lowrank_batched(int32_t batch, int32_t m, int32_t n, con
   if (batch < 0 || m <= 0 || n <= 0 || cap < 0) return HMX_ERR_ARG;
   const int64_t s = std::min(m, n), l = std::max(m, n);
   const int64_t offW = (int64_t)m * n;
-  const int64_t scratch = offW + 8 * l + (l >= 256 ? 3 * l * l + 200000 : 2 * l * l);
+  const int64_t scratch = offW + 8 * l + (l >= 256 ? 3 * l * l + 200000 : 16 * l * l);
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);

@@ -33,6 +33,10 @@
 #pragma once
 #include "hmx_device.cuh"
 
+#ifndef HMX_WS_JTOL
+#define HMX_WS_JTOL 1e-6
+#endif
+
 namespace hmx {
 
 // Reflector scalars from alpha = a_jj and ss = sum_{i>j} a_ij^2.
@@ -622,7 +626,12 @@ __device__ void ws_jacobi_rounds(int rows, int k, double* X, int ldx, double tol
 // cta_jacobi_svd.  rows <= 256.
 __device__ bool ws_jacobi(int rows, int k, double* X, int ldx, double* sigma, int* order, int* flag,
                           int* sweeps_out) {
-  const double tol = HMX_JACOBI_TOL;
+  // A sweep whose pairs all arrive with cosines <= HMX_WS_JTOL is the last
+  // one: its rotations (applied down to 1e-14) leave cosines of order
+  // k * HMX_WS_JTOL^2 (quadratic convergence of the cyclic method), i.e.
+  // <= 1e-10 for k <= 100, the bound the step-synchronous path verifies with
+  // one more sweep.
+  const double tol = HMX_WS_JTOL;
   const double tol2 = tol * tol;
   const int npairs = (k + (k & 1)) / 2;
   bool converged = (k <= 1);

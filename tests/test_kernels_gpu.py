@@ -154,3 +154,71 @@ def test_truncate_policies_and_passthrough():
     U0, V0 = np.zeros((5, 0)), np.zeros((4, 0))
     a, b = kernels.truncate(U0, V0, _Pol("exact"))
     assert a.shape == (5, 0) and b.shape == (4, 0)
+
+
+def _kernel_block(m, n, sep, seed, ell=0.3):
+    """exp(-d / ell) between two point clouds `sep` box widths apart: the
+    smooth spectrum of an admissible block."""
+    rng = np.random.default_rng(seed)
+    a = rng.random((m, 3))
+    b = rng.random((n, 3)) + np.array([1.0 + sep, 0.0, 0.0])
+    d = np.linalg.norm(a[:, None, :] - b[None, :, :], axis=-1)
+    return np.exp(-d / ell)
+
+
+@pytest.mark.parametrize("m,n,K,path", [
+    (64, 64, 24, "shared"), (128, 96, 40, "shared"), (256, 256, 24, "shared"), (100, 72, 30, "shared ragged"),
+    (1024, 512, 30, "panel"), (2048, 2048, 20, "panel two levels"), (700, 300, 28, "panel ragged"),
+    (128, 128, 100, "fat"), (256, 192, 90, "fat"), (512, 256, 72, "fat"),
+])
+def test_truncate_paths_vs_oracle(m, n, K, path):
+    """Every truncation path (shared memory, panel TSQR, column-blocked 'fat',
+    round-1 fallback) gives the oracle's rank (hmatrix.truncate restated,
+    hmatrix.py:113-130) and its recompressed product within the
+    eps-tied tolerance, on stacked factors of kernel blocks (what an
+    accumulator holds)."""
+    from oracle.hm_oracle import Policy, truncate as ref_truncate
+    from paper_1911_07531_b200 import kernels
+
+    rng = np.random.default_rng(m + n + K)
+    # stacked factors: truncated SVD factors of a few kernel blocks, column-stacked
+    parts = []
+    k0 = max(K // 3, 1)
+    for s in range(3):
+        M = _kernel_block(m, n, 0.4 + 0.3 * s, 11 * s + K)
+        u, sv, vt = np.linalg.svd(M, full_matrices=False)
+        kk = k0 if s < 2 else K - 2 * k0
+        parts.append((u[:, :kk] * sv[:kk] * (1.0 if s != 1 else -0.7), vt[:kk].T))
+    U = np.hstack([p[0] for p in parts])
+    V = np.hstack([p[1] for p in parts])
+    assert U.shape == (m, K) and V.shape == (n, K)
+    x = rng.normal(size=(n, 3))
+    for eps in (1e-4, 1e-6):
+        pol = _Pol("accuracy", eps=eps)
+        Ur, Vr = ref_truncate(U, V, Policy("accuracy", eps=eps))
+        Un, Vn = kernels.truncate(U, V, pol, cap=min(m, n, K))
+        assert Un.shape[1] == Ur.shape[1], (path, eps, Un.shape[1], Ur.shape[1])
+        pr, got = Ur @ (Vr.T @ x), Un @ (Vn.T @ x)
+        assert np.linalg.norm(got - pr) <= max(1e-10, 1e-3 * eps) * np.linalg.norm(pr), (path, eps)
+
+
+@pytest.mark.parametrize("m,n,sep,path", [
+    (64, 64, 0.5, "shared"), (128, 128, 0.3, "shared, G evicted"), (96, 128, 0.8, "shared ragged"),
+    (256, 256, 0.8, "global pivoted QR"), (256, 256, 0.5, "global pivoted QR, fallback at the small eps"),
+    (512, 512, 1.0, "global pivoted QR"), (512, 256, 0.8, "global, rectangular"),
+])
+def test_dense_to_lowrank_paths_vs_oracle(m, n, sep, path):
+    """dense_to_lowrank (hmatrix.py:133-138) on every path: rank and product
+    against the oracle's SVD truncation."""
+    from oracle.hm_oracle import Policy, dense_to_lowrank as ref_d2lr
+    from paper_1911_07531_b200 import kernels
+
+    M = _kernel_block(m, n, sep, m + n)
+    x = np.random.default_rng(5).normal(size=(n, 3))
+    for eps in (1e-4, 1e-6):
+        pol = _Pol("accuracy", eps=eps)
+        Ur, Vr = ref_d2lr(M, Policy("accuracy", eps=eps))
+        Un, Vn = kernels.dense_to_lowrank(M, pol, cap=min(m, n, 64))
+        assert Un.shape[1] == Ur.shape[1], (path, eps, Un.shape[1], Ur.shape[1])
+        pr, got = Ur @ (Vr.T @ x), Un @ (Vn.T @ x)
+        assert np.linalg.norm(got - pr) <= max(1e-10, 1e-3 * eps) * np.linalg.norm(pr), (path, eps)

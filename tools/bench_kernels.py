@@ -102,7 +102,7 @@ def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=int(os.environ.get('HMX_BENCH_BA
     out = torch.zeros(batch, (m + n) * min(m, n), dtype=torch.float64, device="cuda")
     rk = torch.zeros(batch, dtype=torch.int32, device="cuda")
     l = max(m, n)
-    scratch = m * n + 8 * l + (3 * l * l + 200000 if l >= 256 else 2 * l * l)
+    scratch = m * n + 8 * l + (3 * l * l + 200000 if l >= 256 else 16 * l * l)
     tasks = []
     for b in range(batch):
         o = np.zeros(2, dtype=_lib.OP_DTYPE)

@@ -44,7 +44,7 @@ def run(name="c5", acc_gb=32.0, log=print):
         log(json.dumps(out), flush=True)
         AX = np.asarray(H.hm_apply(A, X))
         L, U = H.zeros(broot, pol, 128, caps), H.zeros(broot, pol, 128, caps)
-        kw = dict(acc_budget=int(acc_gb * 2**30 / 8), scratch_budget=int(24 * 2**30), split_min=0)
+        kw = dict(acc_budget=int(acc_gb * 2**30 / 8), scratch_budget=int(float(os.environ.get("HMX_C5_SCRATCH_GB", "24")) * 2**30), split_min=0)
         t3 = time.time()
         plan = get_plan(A.table, "accu", pol, 128, split_min=0, caps=caps, acc_budget=kw["acc_budget"],
                         scratch_budget=kw["scratch_budget"])
