@@ -206,6 +206,35 @@ class HStore:
         return out
 
 
+def task_signature(ops, task_ops):
+    """Batch key of every task: (op code, rows, columns) of its heaviest op -
+    the truncation / dense_to_lowrank if it has one, else the LU / TRSM,
+    else its first GEMM, else its first op - packed into one int64."""
+    nt = len(task_ops) - 1
+    if nt == 0:
+        return np.zeros(0, dtype=np.int64)
+    code = ops["code"].astype(np.int64)
+    d0 = np.maximum(ops["dim"][:, 0].astype(np.int64), 0)
+    d1 = np.maximum(ops["dim"][:, 1].astype(np.int64), 0)
+    # priority of an op as the task's representative
+    prio = np.select([np.isin(code, (8, 9)), np.isin(code, (5, 6, 7, 13)), code == 1], [3, 2, 1], 0)
+    key = prio * (1 << 50) + (code << 44) + (np.minimum(d0, (1 << 22) - 1) << 22) + np.minimum(d1, (1 << 22) - 1)
+    starts = np.asarray(task_ops[:-1], dtype=np.int64)
+    empty = np.diff(np.asarray(task_ops, dtype=np.int64)) == 0
+    sig = np.maximum.reduceat(key, np.minimum(starts, len(key) - 1)) if len(key) else np.zeros(nt, np.int64)
+    sig = np.where(empty, 0, sig)
+    return sig & ((1 << 50) - 1)
+
+
+def wave_batches(levels, ops, task_ops):
+    """Task order of the ASAP wavefronts with every wavefront sorted into
+    batches of equal signature (operation type and leaf shape).  Returns
+    (order, signature per task)."""
+    sig = task_signature(ops, task_ops)
+    order = np.lexsort((sig, np.asarray(levels))).astype(np.int32)
+    return order, sig
+
+
 class ExecPlan:
     """Lowered H-LU plan + its device execution graph."""
 
@@ -272,7 +301,9 @@ class ExecPlan:
                                  [[ne * self.nrep]]).astype(np.int32)
             idx = np.concatenate([idx + b * nt for b in range(self.nrep)]).astype(np.int32)
             lv = np.tile(lv, self.nrep)
-        order = np.argsort(lv, kind="stable").astype(np.int32)
+        # ready-set wavefronts; inside a wavefront the tasks are grouped into
+        # batches of equal operation type and leaf shape (wave_batches)
+        order, self.batch_sig = wave_batches(lv, ops, task_ops)
         counts = np.bincount(lv, minlength=int(lv.max()) + 1 if len(lv) else 1)
         self.wave_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self.wave_tasks = order
@@ -397,7 +428,11 @@ class ExecPlan:
 
     def stats(self):
         w = np.diff(self.wave_ptr)
+        lv_sig = np.stack([np.asarray(self.levels, dtype=np.int64), self.batch_sig[:len(self.levels)]], 1) \
+            if len(self.levels) else np.zeros((0, 2), np.int64)
+        n_batches = int(len(np.unique(lv_sig, axis=0))) if self.n_tasks <= 500000 else -1
         return {"tasks": self.n_tasks, "ops": int(len(self.prog.ops)), "dag_edges": self.n_dag_edges,
+                "batches": n_batches,
                 "exec_edges": int(len(self.succ_idx)), "dataflow_only_edges": self.n_chain_edges, "waves": int(len(w)),
                 "max_wave": int(w.max()) if len(w) else 0,
                 "scratch_mb_per_cta": self.prog.scratch_doubles * 8 / 2**20,

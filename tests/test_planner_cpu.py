@@ -101,3 +101,34 @@ def test_replicate_shifts_refs_and_slots():
                     assert (int(r1) & m56) == (int(r0) & m56) + c * sizes[base]
                 else:
                     assert r1 == r0
+
+
+def test_wavefront_batches_group_by_op_type_and_leaf_shape():
+    """engine.wave_batches: the ASAP wavefronts stay intact and inside every
+    wavefront tasks of equal signature (op type, leaf shape) are contiguous."""
+    from paper_1911_07531_b200 import taskgraph as tg
+    from paper_1911_07531_b200.engine import wave_batches
+
+    cfg, bt = case("s2")
+    prog = planner.plan_hlu(bt, "accu", Policy("accuracy", eps=cfg.eps), rank_cap=64)
+    nt = len(prog.task_ops) - 1
+    from paper_1911_07531_b200.planner import dataflow_edges
+
+    e = np.array(sorted(dataflow_edges(prog, {0: bt, 1: bt, 2: bt})), dtype=np.int64).reshape(-1, 2)
+    ptr = np.zeros(nt + 1, dtype=np.int32)
+    np.add.at(ptr, e[:, 0] + 1, 1)
+    ptr = np.cumsum(ptr).astype(np.int32)
+    idx = e[np.argsort(e[:, 0], kind="stable"), 1].astype(np.int32)
+    lv = tg.asap_levels(nt, ptr, idx)
+    order, sig = wave_batches(lv, prog.ops, prog.task_ops)
+    assert sorted(order.tolist()) == list(range(nt))
+    lo = lv[order]
+    assert (np.diff(lo) >= 0).all()
+    so = sig[order]
+    same = np.diff(lo) == 0
+    assert (np.diff(so)[same] >= 0).all()          # sorted inside a wavefront: batches are contiguous
+    nb = len(np.unique(np.stack([lo, so], 1), axis=0))
+    assert nb < nt                                   # tasks do share batches
+    # a truncating task is keyed by its truncation: op code 8 or 9 in the signature
+    codes = set((so >> 44).tolist())
+    assert codes & {8, 9}

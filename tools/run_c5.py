@@ -45,6 +45,9 @@ def run(name="c5", acc_gb=32.0, log=print):
         AX = np.asarray(H.hm_apply(A, X))
         L, U = H.zeros(broot, pol, 128, caps), H.zeros(broot, pol, 128, caps)
         kw = dict(acc_budget=int(acc_gb * 2**30 / 8), scratch_budget=int(float(os.environ.get("HMX_C5_SCRATCH_GB", "24")) * 2**30), split_min=0)
+        torch.cuda.empty_cache()  # plan_create allocates with cudaMalloc: release torch's cached blocks
+        out.update(mem_before_plan_gb=torch.cuda.memory_allocated() / 2**30,
+                   mem_reserved_gb=torch.cuda.memory_reserved() / 2**30)
         t3 = time.time()
         plan = get_plan(A.table, "accu", pol, 128, split_min=0, caps=caps, acc_budget=kw["acc_budget"],
                         scratch_budget=kw["scratch_budget"])
