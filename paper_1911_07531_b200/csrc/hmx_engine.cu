@@ -292,6 +292,9 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
   }
 }
 
+#ifndef HMX_GWIDE
+#define HMX_GWIDE 0
+#endif
 #ifndef HMX_WS
 #define HMX_WS 3  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path, 3: + fat path
 #endif
@@ -1294,8 +1297,14 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
                    mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
       else
 #endif
+#if HMX_GWIDE
+      // shape-adaptive tiles (128x32 / 32x128 / split-k) for the skinny products
+      cta_gemm_wide(m, n, k, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
+                    mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
+#else
       cta_gemm(m, n, k, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
                mref(P, c, o.ref[1]), o.ld[1], o.flags & F_TB, acc, C, o.ld[2], work);
+#endif
       count(P, 2.0 * m * n * k, 8.0 * ((double)m * k + (double)k * n + (double)m * n));
       break;
     }

@@ -4,6 +4,8 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 O=gpurun_out/$1; mkdir -p $O
 nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 1800 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err; echo "rc=$?" >> $O/bench_c3.err
 for cfg in c2 c1 c4 c5_d3; do
   timeout 1200 python bench.py --config $cfg > $O/bench_$cfg.json 2> $O/bench_$cfg.err; echo "rc=$?" >> $O/bench_$cfg.err
@@ -15,6 +17,11 @@ for v in "" _dmma; do
   HMX_LIB=$lib timeout 600 python tools/ab_gemm.py > $O/ab_gemm$v.log 2>&1
   HMX_LIB=$lib timeout 900 python bench.py --config c2 --no-cpu-baseline --no-e2e > $O/ab_c2$v.json 2> $O/ab_c2$v.err
 done
+# A/B: shape-adaptive GEMM tiles in the op interpreter
+HMX_LIB=$PWD/paper_1911_07531_b200/libhmx_gwide.so timeout 900 python bench.py --config c3 --no-cpu-baseline --no-e2e > $O/ab_c3_gwide.json 2> $O/ab_c3_gwide.err
+HMX_LIB=$PWD/paper_1911_07531_b200/libhmx_gwide.so timeout 900 python bench.py --config c2 --no-cpu-baseline --no-e2e > $O/ab_c2_gwide.json 2> $O/ab_c2_gwide.err
+timeout 900 python tools/trace_case.py c2 > $O/trace_c2.txt 2>&1
+timeout 900 python tools/trace_case.py c3 > $O/trace_c3.txt 2>&1
 # profiler passes (after the plain runs above exited)
 timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_|hmx" --csv \
   --log-file $O/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
