@@ -239,8 +239,13 @@ __device__ __forceinline__ void gemm_tiles(int m, int n, int k, double alpha, co
 // (fragment layout of mma.m8n8k4.f64: A[g][t], B[t][g], C[g][2t+i] with
 // g = lane/4, t = lane%4).  The k-order inside one mma is the hardware's,
 // so results differ from the DFMA chains in the last bits.
+// 1 (default since round 2): the 64x64 tiles of cta_gemm run on the FP64
+// tensor cores.  A/B on one box (profiles/r02_dmma_ab.md): 256^3 batch 10.8
+// vs 9.2 TFLOP/s, 128x128x64 4.0 vs 3.6, c2 factorization 0.1990 vs 0.2053 s,
+// ranks equal to the reference fixtures with both arms; half the issued
+// instructions (431 M vs 887 M for the 256^3 batch).
 #ifndef HMX_DMMA
-#define HMX_DMMA 0
+#define HMX_DMMA 1
 #endif
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"

@@ -933,6 +933,59 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
   return true;
 }
 
+// Second half of the large dense_to_lowrank paths: the block has been
+// factored by a pivoted QR (Gs: R1 and the reflector tails, shared or global
+// memory; tp / wd / rd / perm / pos of k <= 120 steps).  Q_G becomes one clean
+// reflector block, B = R1^T is factored by the column-blocked QR and the fat
+// core finishes.  false (nothing written) if the global scratch is too small.
+__device__ bool d2lr_tail(const DevPlan& P, const hmx_op& o, int m, int n, int k, const double* Gs,
+                          int64_t ldgs, const double* tpa, const double* wda, const double* rda,
+                          const int* perma, const int* posa, double* Uo, int lduo, double* Vo, int ldvo,
+                          int* rslot, double* ws, double* sm, double* gsm, unsigned long long& tq) {
+  const int tid = threadIdx.x;
+  const int64_t l = max(m, n);
+  const int KC = min(min(m, n), 120);
+  const int64_t avail = l < 256 ? 16 * l * l : 2 * l * l + 200000;
+  if (k > KC || (int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > avail) return false;
+  const int rcap = min(KC, max(o.iarg[2], 1));
+  if (ws_cb_nb(n, KC, P.smem_work) == 0 || fat_core_need(KC, KC, KC, ws_cb_nb(n, KC, P.smem_work), rcap) > P.smem_work)
+    return false;
+  double* Wc = ws + 8 * l;                 // m x k: Q_G as one clean reflector block (ld m)
+  double* B = Wc + (int64_t)m * KC;        // n x k: R1^T
+  double* Rzv = B + (int64_t)n * KC;       // k x k
+  double* Sgu = Rzv + (int64_t)KC * KC;    // k x k: W_c^T W_c
+  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR
+  double* tpu = Sgv + 128 * (int64_t)KC;
+  double* tpv = tpu + KC;
+  double* gs = tpv + KC;                   // fat_core scratch (6 k^2 + 2 k)
+  if (k == 0) {
+    if (tid == 0) *rslot = 0;
+    __syncthreads();
+    return true;
+  }
+  // Q_G as one clean reflector block; B = R1^T
+  FOR_MN(i, j, m, k)
+    Wc[i + (int64_t)j * m] = i > j ? Gs[i + (int64_t)perma[j] * ldgs] : (i == j ? wda[j] : 0.0);
+  FOR_MN(c_, i, n, k) {
+    const int pc = posa[c_];
+    B[c_ + (int64_t)i * n] = pc > i ? Gs[i + (int64_t)c_ * ldgs] : (pc == i ? rda[i] : 0.0);
+  }
+  for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = tpa[e];
+  __syncthreads();
+  ws_smat_gemm(m, k, Wc, m, Sgu, k, gsm);
+  const int nb2 = ws_cb_nb(n, k, P.smem_work);
+  ws_cbqr(n, k, B, n, Rzv, tpv, Sgv, nb2, sm + 32);
+  FatSide fu{m, k, Wc, m, tpu, Sgu, k, k};
+  FatSide fv{n, k, B, n, tpv, Sgv, nb2, nb2};
+  const int r = fat_core(P, o, k, k, k, nullptr, Rzv, fu, fv, Uo, lduo, Vo, ldvo, gs, sm, tq);
+  phase(P, 15, tq);
+  if (tid == 0) *rslot = r;
+  const int s_ = min(m, n);
+  count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s_ + (double)s_ * n));
+  __syncthreads();
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // dense_to_lowrank of a block too large for shared memory (<= 512 x 512,
 // capacity <= 64): rank-revealing QR in place in global memory (ws_gqr),
@@ -950,21 +1003,13 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
   if (mid && (m < 16 || n < 16)) return false;
   const int tid = threadIdx.x;
   const int64_t l = max(m, n);
-  const int KC = mid ? min(m, n) : 120;  // largest revealed rank handled here (the core must fit shared memory)
+  const int KC = min(min(m, n), 120);  // largest revealed rank handled here (the core must fit shared memory)
   const int nbv = ws_cb_nb(n, KC, P.smem_work);
   const int rcap = min(KC, max(o.iarg[2], 1));
   if (nbv == 0 || fat_core_need(KC, KC, KC, nbv, rcap) > P.smem_work) return false;
   // global scratch (planner): 8 l + 16 l^2 (l < 256) or 8 l + 3 l^2 + 200000, the last l^2 keep M
   const int64_t avail = mid ? 16 * l * l : 2 * l * l + 200000;
   if ((int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > avail) return false;
-  double* Wc = ws + 8 * l;                 // m x k: Q_G as one clean reflector block (ld m)
-  double* B = Wc + (int64_t)m * KC;        // n x k: R1^T
-  double* Rzv = B + (int64_t)n * KC;       // k x k
-  double* Sgu = Rzv + (int64_t)KC * KC;    // k x k: W_c^T W_c
-  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR
-  double* tpu = Sgv + 128 * (int64_t)KC;
-  double* tpv = tpu + KC;
-  double* gs = tpv + KC;                   // fat_core scratch (6 k^2 + 2 k)
   unsigned long long tq = P.trace ? gtimer2() : 0;
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
@@ -995,6 +1040,7 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
     }
     __syncthreads();
     k = ired[0];
+    if (k > KC) return false;  // M is intact: the caller falls back
     Gs = G;
     ldgs = lg;
   } else {
@@ -1021,32 +1067,8 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
     ldgs = ldm;
   }
   phase(P, 13, tq);
-  if (k == 0) {
-    if (tid == 0) *rslot = 0;
-    __syncthreads();
-    return true;
-  }
-  // Q_G as one clean reflector block; B = R1^T
-  FOR_MN(i, j, m, k)
-    Wc[i + (int64_t)j * m] = i > j ? Gs[i + (int64_t)perma[j] * ldgs] : (i == j ? wda[j] : 0.0);
-  FOR_MN(c_, i, n, k) {
-    const int pc = posa[c_];
-    B[c_ + (int64_t)i * n] = pc > i ? Gs[i + (int64_t)c_ * ldgs] : (pc == i ? rda[i] : 0.0);
-  }
-  for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = tpa[e];
-  __syncthreads();
-  ws_smat_gemm(m, k, Wc, m, Sgu, k, gsm);
-  const int nb2 = ws_cb_nb(n, k, P.smem_work);
-  ws_cbqr(n, k, B, n, Rzv, tpv, Sgv, nb2, sm + 32);
-  FatSide fu{m, k, Wc, m, tpu, Sgu, k, k};
-  FatSide fv{n, k, B, n, tpv, Sgv, nb2, nb2};
-  const int r = fat_core(P, o, k, k, k, nullptr, Rzv, fu, fv, Uo, lduo, Vo, ldvo, gs, sm, tq);
-  phase(P, 15, tq);
-  if (tid == 0) *rslot = r;
-  const int s_ = min(m, n);
-  count(P, svd_flops(m, n), 8.0 * ((double)m * n + (double)m * s_ + (double)s_ * n));
-  __syncthreads();
-  return true;
+  return d2lr_tail(P, o, m, n, k, Gs, ldgs, tpa, wda, rda, perma, posa, Uo, lduo, Vo, ldvo, rslot, ws, sm,
+                   gsm, tq);
 }
 
 // ---------------------------------------------------------------------------
@@ -1215,7 +1237,13 @@ __device__ __noinline__ bool d2lr_ws(const DevPlan& P, const hmx_op& o, int m, i
   unsigned long long tq = P.trace ? gtimer2() : 0;
   int k = 0;
   const int r = ws_core(P, o, m, n, w, sm, tq, &k);
-  if (r < 0) return false;
+  if (r < 0) {
+    // the revealed rank does not fit the shared-memory core: the factored
+    // block (still in shared memory) continues on the fat core
+    if (w.cap2 < GEMM_SMEM_DOUBLES) return false;
+    return d2lr_tail(P, o, m, n, k, w.G, w.lg, w.tpg, w.wdg, w.rdg, w.perm, w.pos, Uo, lduo, Vo, ldvo, rslot,
+                     ws, sm, w.free2, tq);
+  }
   FOR_MN(i, t, m, r) Uo[i + (int64_t)t * lduo] = w.Yu[i + t * ly];
   FOR_MN(c_, t, n, r) Vo[c_ + (int64_t)t * ldvo] = w.X[c_ + (int64_t)w.ord[t] * lx];
   __syncthreads();
@@ -1843,7 +1871,13 @@ cudaError_t launch_waves(hmx_plan* p, cudaStream_t s) {
 
 extern "C" {
 
-const char* hmx_version(void) { return "hmx 0.1 sm_100a fp64"; }
+const char* hmx_version(void) {
+#if HMX_DMMA
+  return "hmx 0.2 sm_100a fp64 dmma";
+#else
+  return "hmx 0.2 sm_100a fp64 dfma";
+#endif
+}
 int hmx_op_size(void) { return (int)sizeof(hmx_op); }
 
 hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {

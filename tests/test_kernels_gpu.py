@@ -83,7 +83,7 @@ def test_gemm_small_path_bitwise_equals_tiled(ta, tb):
     64x64 tiled GEMM run the same increasing-k fma chain per output: a
     sub-block computed alone (small path) equals the same entries of a large
     product (tiled path) bit for bit."""
-    from paper_1911_07531_b200 import kernels
+    from paper_1911_07531_b200 import _lib, kernels
 
     rng = np.random.default_rng(11)
     m, n, k = 96, 80, 45
@@ -96,7 +96,12 @@ def test_gemm_small_path_bitwise_equals_tiled(ta, tb):
         Bs = B[j0:j1, :] if tb else B[:, j0:j1]
         sub = kernels.gemm(-0.7, [np.ascontiguousarray(As)], [np.ascontiguousarray(Bs)],
                            [np.ascontiguousarray(C0[i0:i1, j0:j1])], transA=ta, transB=tb, beta=1.0)[0]
-        assert np.array_equal(sub, big[i0:i1, j0:j1])
+        if b"dmma" in _lib.lib().hmx_version():
+            # the tiled path runs on the FP64 tensor cores (k summed in the mma's
+            # order): the two paths agree to rounding, not bit for bit
+            assert np.abs(sub - big[i0:i1, j0:j1]).max() <= 1e-13 * np.abs(big).max()
+        else:
+            assert np.array_equal(sub, big[i0:i1, j0:j1])
 
 
 class _Pol:
