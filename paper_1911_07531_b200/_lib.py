@@ -46,6 +46,21 @@ class HmxError(RuntimeError):
         super().__init__(f"hmx {what}: status {self.code} ({', '.join(names) or 'ok'})")
 
 
+def d2lr_scratch(m: int, n: int) -> int:
+    """Workspace (doubles) an OP_D2LR of an m x n block needs (op.wref): the
+    warp-synchronous / global pivoted-QR paths of hmx_engine.cu keep their
+    reflector blocks, R1^T, the fat core's scratch and (blocks of 256 and
+    more) a copy of the block there.  hmx_lower.cpp uses the same formula."""
+    l = max(int(m), int(n))
+    return 8 * l + (3 * l * l + 2500000 if l >= 256 else 16 * l * l)
+
+
+def trunc_scratch(m: int, n: int, kb: int) -> int:
+    """Workspace (doubles) of an OP_TRUNC with stacked capacity kb."""
+    kb = max(int(kb), 1)
+    return 9 * kb * kb + (int(m) + int(n) + 200) * kb + 2048
+
+
 def mref(base: int, off: int) -> int:
     return (int(base) << 56) | int(off)
 

@@ -159,7 +159,7 @@ def _compress_small(values, ranks_d, u_off, v_off, cap, tmp, tmp_off, items, pol
     for i, u in enumerate(items):
         m, n = int(t.m[u]), int(t.nc[u])
         l = max(m, n)
-        ws = max(ws, 8 * l + 2 * l * l)
+        ws = max(ws, _lib.d2lr_scratch(m, n))
         o = ops[i]
         o["code"] = OP_D2LR
         o["dim"][:2] = (m, n)

@@ -786,19 +786,31 @@ __device__ void fat_apply(const FatSide& f, const double* Yin, int64_t ldy, int 
   }
 }
 
+// Reflectors of the core's pivoted QR are applied in blocks of this width
+constexpr int FAT_NBQ = 80;
+// cores up to this size keep G / X in shared memory; larger ones (<= 256)
+// run from global scratch (L2)
+constexpr int FAT_SMEM_CORE = 120;
+
 // shared work the fat core needs (doubles) for a p x q core, block widths
 // nbu / nbv of the outer factors, rank cap rcap
 __device__ __forceinline__ int64_t fat_core_need(int p, int q, int nbu, int nbv, int rcap) {
   const int l = max(p, q), s = min(p, q);
-  const int nbw = max(max(nbu, nbv), s);
-  const int64_t a = (int64_t)(l | 1) * l;  // G / X
+  const int nbw = max(max(nbu, nbv), min(s, FAT_NBQ));
+  const int64_t a = l <= FAT_SMEM_CORE ? (int64_t)(l | 1) * l : 0;  // G / X in shared memory
   const int64_t b = (int64_t)(nbw | 1) * nbw + (int64_t)(nbw | 1) * rcap + nbw + GEMM_SMEM_DOUBLES;  // Sc, Bm, sw, gsm
-  return max(a, b) + 7 * (int64_t)q + 96;
+  const int64_t c = q > 256 ? 4 * (int64_t)q + 2 * (int64_t)p + 64 : 0;  // ws_gqr's arrays of a large core
+  return max(max(a, b), c) + 7 * (int64_t)q + 128;
+}
+// global scratch of the fat core (doubles)
+__device__ __forceinline__ int64_t fat_core_gs(int p, int q) {
+  const int64_t l = max(p, q);
+  return 6 * l * l + 2 * l + (l > FAT_SMEM_CORE ? 2 * (l | 1) * l : 0);
 }
 
 // Core and recomposition.  Ru (p x Kc, ld p) and Rv (q x Kc, ld q) in global
-// (Ru == nullptr: the identity, p == Kc).  gs: global scratch of at least
-// 6 max(p,q)^2 + 2 max(p,q) doubles.  Returns r; Uo / Vo written.
+// (Ru == nullptr: the identity, p == Kc).  gs: global scratch of
+// fat_core_gs(p, q) doubles.  p, q <= 512.  Returns r; Uo / Vo written.
 __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc, const double* Ru,
                         const double* Rv, const FatSide& fu, const FatSide& fv, double* Uo, int lduo,
                         double* Vo, int ldvo, double* gs, double* sm, unsigned long long& tq) {
@@ -806,6 +818,7 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
   int* flag = reinterpret_cast<int*>(sm + 24);
   const int tid = threadIdx.x;
   const int l = max(p, q);
+  const bool xl = l > FAT_SMEM_CORE;
   const int lg = p | 1, lx = q | 1;
   double* wp = sm + 32;
   auto take = [&](int64_t nd) { double* r_ = wp; wp += nd; return r_; };
@@ -813,9 +826,18 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
   int* perm = reinterpret_cast<int*>(take(q));
   int* pos = perm + q;
   int* ord = reinterpret_cast<int*>(take(q));
-  double* xr = take(32);
-  double* big = wp;  // G, then X, then the block-apply work (Sc, Bm, sw, gsm)
-  double* G = big;
+  double* xr = take(64);
+  double* big = wp;  // (G, then X), then the block-apply work (Sc, Bm, sw, gsm)
+  const int64_t l2 = (int64_t)l * l;
+  double* X0 = gs;              // q x k (ld q): R1^T before the rotations
+  double* Yu = X0 + l2;         // p x r (ld p)
+  double* Yv = Yu + l2;         // q x r (ld q)
+  double* Wc = Yv + l2;         // p x k (ld p): Q_G as clean reflector blocks
+  double* Sq = Wc + l2;         // per block of FAT_NBQ reflectors: W_c^T W_c (ld FAT_NBQ)
+  double* Xs = Sq + l2;         // q x r (ld q): kept columns of X
+  double* tpq = Xs + l2;        // k
+  double* gbig = tpq + 2 * l;   // G and X of a large core
+  double* G = xl ? gbig : big;
   FOR_MN(i, j, p, q) {
     const int l0 = max(i, j);
     G[i + j * lg] = Ru ? ws_dot<4>(Ru + i + (int64_t)l0 * p, p, Rv + j + (int64_t)l0 * q, q, Kc - l0)
@@ -826,24 +848,27 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
   const double thr = HMX_RRQR_THR * cut;
-  const int nwr = (q + 31) >> 5;
-  if ((tid >> 5) < nwr) {
-    const int k = ws_rrqr(p, q, G, lg, tpg, wdg, rdg, perm, pos, thr, xr, 0, nwr, 3);
-    if (tid == 0) ired[0] = k;
+  if (q <= 256) {
+    const int nwr = (q + 31) >> 5;
+    if ((tid >> 5) < nwr) {
+      const int kk = ws_rrqr(p, q, G, lg, tpg, wdg, rdg, perm, pos, thr, xr, 0, nwr, 3);
+      if (tid == 0) ired[0] = kk;
+    }
+    __syncthreads();
+  } else {
+    // a core above 256 columns: the global pivoted QR (G lives in global scratch)
+    WsGqr a;
+    a.tp = tpg; a.wd = wdg; a.rd = rdg; a.perm = perm; a.pos = pos;
+    a.cn = big; a.gq = a.cn + q; a.rown = a.gq + q; a.fq = a.rown + q;
+    a.wv = a.fq + q; a.wn = a.wv + p; a.red = a.wn + p;
+    __syncthreads();
+    const int kk = p <= 256 ? ws_gqr<8>(p, q, G, lg, thr, min(p, q), a) : ws_gqr<16>(p, q, G, lg, thr, min(p, q), a);
+    if (tid == 0) ired[0] = kk;
+    __syncthreads();
   }
-  __syncthreads();
   const int k = ired[0];
   phase(P, 13, tq);
-  // global scratch
-  const int64_t l2 = (int64_t)l * l;
-  double* X0 = gs;              // q x k (ld q): R1^T before the rotations
-  double* Yu = X0 + l2;         // p x r (ld p)
-  double* Yv = Yu + l2;         // q x r (ld q)
-  double* Wc = Yv + l2;         // p x k (ld p): Q_G as one clean reflector block
-  double* Sq = Wc + l2;         // k x k (ld k): W_c^T W_c
-  double* Xs = Sq + l2;         // q x r (ld q): kept columns of X
-  double* tpq = Xs + l2;        // k
-  // the clean reflector block of Q_G and R1^T leave G before X takes its storage
+  // the clean reflector blocks of Q_G and R1^T leave G before X may take its storage
   FOR_MN(i, j, p, k) {
     const int pc = perm[j];
     Wc[i + (int64_t)j * p] = i > j ? G[i + pc * lg] : (i == j ? wdg[j] : 0.0);
@@ -854,7 +879,7 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
   }
   for (int e = tid; e < k; e += HMX_THREADS) tpq[e] = tpg[e];
   __syncthreads();
-  double* X = big;  // q x k (shared)
+  double* X = xl ? gbig + (int64_t)(l | 1) * l : big;  // q x k
   FOR_MN(c, i, q, k) X[c + i * lx] = X0[c + (int64_t)i * q];
   __syncthreads();
   int sweeps = 0;
@@ -868,10 +893,11 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
     r = cap;
   }
   if (r == 0) return 0;
-  // kept columns of X (unscaled) to global, then X's storage is the work area
+  // kept columns of X (unscaled) to global, then the shared storage is the work area
   FOR_MN(c, t, q, r) Xs[c + (int64_t)t * q] = X[c + (int64_t)ord[t] * lx];
   __syncthreads();
-  const int nbw = max(max(min(fu.nb, fu.p), min(fv.nb, fv.p)), k);
+  const int nbq = min(k, FAT_NBQ);
+  const int nbw = max(max(min(fu.nb, fu.p), min(fv.nb, fv.p)), nbq);
   double* Sc = big;
   double* Bm = Sc + (int64_t)(nbw | 1) * nbw;
   double* sw = Bm + (int64_t)(nbw | 1) * r;
@@ -883,9 +909,17 @@ __device__ int fat_core(const DevPlan& P, const hmx_op& o, int p, int q, int Kc,
     Yu[i + (int64_t)t * p] = i < k ? Yu[i + (int64_t)t * p] / sg : 0.0;
   }
   FOR_MN(c, t, q, r) Yv[c + (int64_t)t * q] = Xs[c + (int64_t)t * q] / sig[ord[t]];
-  ws_smat_gemm(p, k, Wc, p, Sq, k, gsm);
-  // Yu := Q_G Yu
-  ws_apply_block(p, k, Wc, p, tpq, Sq, k, false, Yu, p, r, Sc, Bm, sw, gsm);
+  // Yu := Q_G Yu, block by block (last block first)
+  const int nblk = (k + nbq - 1) / nbq;
+  for (int b = 0; b < nblk; ++b) {
+    const int c0 = b * nbq, jc = min(nbq, k - c0);
+    ws_smat_gemm(p - c0, jc, Wc + c0 + (int64_t)c0 * p, p, Sq + (int64_t)b * FAT_NBQ * FAT_NBQ, FAT_NBQ, gsm);
+  }
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int c0 = b * nbq, jc = min(nbq, k - c0);
+    ws_apply_block(p - c0, jc, Wc + c0 + (int64_t)c0 * p, p, tpq + c0, Sq + (int64_t)b * FAT_NBQ * FAT_NBQ,
+                   FAT_NBQ, false, Yu + c0, p, r, Sc, Bm, sw, gsm);
+  }
   fat_apply(fu, Yu, p, r, Uo, lduo, Sc, Bm, sw, gsm);
   fat_apply(fv, Yv, q, r, Vo, ldvo, Sc, Bm, sw, gsm);
   __syncthreads();
@@ -907,7 +941,7 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
   // global workspace (planner: 9 kb^2 + (m + n + 200) kb + 2048 doubles):
   // R_u, R_v, tp (2 K), the per-block S of both factors (<= 2 * 128 K), fat_core's 6 l^2 + 2 l
   const int64_t l = max(p, q);
-  if (kb < K || 2 * (int64_t)K * K + 2 * (int64_t)K + 256 * (int64_t)K + 6 * l * l + 2 * l >
+  if (kb < K || 2 * (int64_t)K * K + 2 * (int64_t)K + 256 * (int64_t)K + fat_core_gs(p, q) >
                     9 * kb * kb + 200 * kb + 2048)
     return false;
   double* Rzu = ws;
@@ -933,6 +967,20 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
   return true;
 }
 
+// largest revealed rank of the large dense_to_lowrank paths and the extra global
+// scratch the planner grants blocks of 256 and more (doubles)
+#ifndef HMX_D2LR_HANDOFF
+#define HMX_D2LR_HANDOFF 1
+#endif
+#ifndef HMX_D2LR_BIG
+#define HMX_D2LR_BIG 1
+#endif
+#ifndef HMX_D2LR_KC
+#define HMX_D2LR_KC 480
+#endif
+constexpr int D2LR_KC = HMX_D2LR_KC;
+constexpr int64_t D2LR_EXTRA = 2500000;
+
 // Second half of the large dense_to_lowrank paths: the block has been
 // factored by a pivoted QR (Gs: R1 and the reflector tails, shared or global
 // memory; tp / wd / rd / perm / pos of k <= 120 steps).  Q_G becomes one clean
@@ -944,26 +992,28 @@ __device__ bool d2lr_tail(const DevPlan& P, const hmx_op& o, int m, int n, int k
                           int* rslot, double* ws, double* sm, double* gsm, unsigned long long& tq) {
   const int tid = threadIdx.x;
   const int64_t l = max(m, n);
-  const int KC = min(min(m, n), 120);
-  const int64_t avail = l < 256 ? 16 * l * l : 2 * l * l + 200000;
-  if (k > KC || (int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > avail) return false;
-  const int rcap = min(KC, max(o.iarg[2], 1));
-  if (ws_cb_nb(n, KC, P.smem_work) == 0 || fat_core_need(KC, KC, KC, ws_cb_nb(n, KC, P.smem_work), rcap) > P.smem_work)
+  const int KC = min(min(m, n), D2LR_KC);
+  const int64_t avail = l < 256 ? 16 * l * l : 2 * l * l + D2LR_EXTRA;
+  const int64_t sgu = (int64_t)((KC + FAT_NBQ - 1) / FAT_NBQ) * FAT_NBQ * FAT_NBQ;
+  if (k > KC || (int64_t)(m + n) * KC + (int64_t)KC * KC + sgu + 130 * (int64_t)KC + fat_core_gs(KC, KC) > avail)
     return false;
-  double* Wc = ws + 8 * l;                 // m x k: Q_G as one clean reflector block (ld m)
+  const int rcap = min(KC, max(o.iarg[2], 1));
+  const int nbv = ws_cb_nb(n, KC, P.smem_work);
+  if (nbv == 0 || fat_core_need(KC, KC, min(KC, FAT_NBQ), nbv, rcap) > P.smem_work) return false;
+  double* Wc = ws + 8 * l;                 // m x k: Q_G as clean reflector blocks (ld m)
   double* B = Wc + (int64_t)m * KC;        // n x k: R1^T
   double* Rzv = B + (int64_t)n * KC;       // k x k
-  double* Sgu = Rzv + (int64_t)KC * KC;    // k x k: W_c^T W_c
-  double* Sgv = Sgu + (int64_t)KC * KC;    // per-block S of B's QR
+  double* Sgu = Rzv + (int64_t)KC * KC;    // W_c^T W_c per block of FAT_NBQ reflectors (ld FAT_NBQ)
+  double* Sgv = Sgu + sgu;                 // per-block S of B's QR
   double* tpu = Sgv + 128 * (int64_t)KC;
   double* tpv = tpu + KC;
-  double* gs = tpv + KC;                   // fat_core scratch (6 k^2 + 2 k)
+  double* gs = tpv + KC;                   // fat_core scratch
   if (k == 0) {
     if (tid == 0) *rslot = 0;
     __syncthreads();
     return true;
   }
-  // Q_G as one clean reflector block; B = R1^T
+  // Q_G as clean reflector blocks; B = R1^T
   FOR_MN(i, j, m, k)
     Wc[i + (int64_t)j * m] = i > j ? Gs[i + (int64_t)perma[j] * ldgs] : (i == j ? wda[j] : 0.0);
   FOR_MN(c_, i, n, k) {
@@ -972,10 +1022,13 @@ __device__ bool d2lr_tail(const DevPlan& P, const hmx_op& o, int m, int n, int k
   }
   for (int e = tid; e < k; e += HMX_THREADS) tpu[e] = tpa[e];
   __syncthreads();
-  ws_smat_gemm(m, k, Wc, m, Sgu, k, gsm);
+  const int nbq = min(k, FAT_NBQ);
+  for (int c0 = 0, b = 0; c0 < k; c0 += nbq, ++b)
+    ws_smat_gemm(m - c0, min(nbq, k - c0), Wc + c0 + (int64_t)c0 * m, m, Sgu + (int64_t)b * FAT_NBQ * FAT_NBQ,
+                 FAT_NBQ, gsm);
   const int nb2 = ws_cb_nb(n, k, P.smem_work);
   ws_cbqr(n, k, B, n, Rzv, tpv, Sgv, nb2, sm + 32);
-  FatSide fu{m, k, Wc, m, tpu, Sgu, k, k};
+  FatSide fu{m, k, Wc, m, tpu, Sgu, FAT_NBQ, nbq};
   FatSide fv{n, k, B, n, tpv, Sgv, nb2, nb2};
   const int r = fat_core(P, o, k, k, k, nullptr, Rzv, fu, fv, Uo, lduo, Vo, ldvo, gs, sm, tq);
   phase(P, 15, tq);
@@ -999,17 +1052,19 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
                                       double* Uo, int lduo, double* Vo, int ldvo, int* rslot, double* ws,
                                       double* sm) {
   const bool mid = m <= 128 && n <= 128;  // pivoted QR in shared memory (M stays intact)
-  if (!mid && (m > 512 || n > 512 || m < 256 || n < 256)) return false;
+  if (!mid && (m > 1024 || n > 1024 || m < 256 || n < 256)) return false;
   if (mid && (m < 16 || n < 16)) return false;
   const int tid = threadIdx.x;
   const int64_t l = max(m, n);
-  const int KC = min(min(m, n), 120);  // largest revealed rank handled here (the core must fit shared memory)
+  const int KC = min(min(m, n), D2LR_KC);  // largest revealed rank handled here
   const int nbv = ws_cb_nb(n, KC, P.smem_work);
   const int rcap = min(KC, max(o.iarg[2], 1));
-  if (nbv == 0 || fat_core_need(KC, KC, KC, nbv, rcap) > P.smem_work) return false;
-  // global scratch (planner): 8 l + 16 l^2 (l < 256) or 8 l + 3 l^2 + 200000, the last l^2 keep M
-  const int64_t avail = mid ? 16 * l * l : 2 * l * l + 200000;
-  if ((int64_t)(m + n) * KC + 9 * (int64_t)KC * KC + 132 * KC > avail) return false;
+  if (nbv == 0 || fat_core_need(KC, KC, min(KC, FAT_NBQ), nbv, rcap) > P.smem_work) return false;
+  // global scratch (planner): 8 l + 16 l^2 (l < 256) or 8 l + 3 l^2 + D2LR_EXTRA, the last l^2 keep M
+  const int64_t avail = mid ? 16 * l * l : 2 * l * l + D2LR_EXTRA;
+  if ((int64_t)(m + n) * KC + (int64_t)KC * KC + (int64_t)((KC + FAT_NBQ - 1) / FAT_NBQ) * FAT_NBQ * FAT_NBQ +
+          130 * (int64_t)KC + fat_core_gs(KC, KC) > avail)
+    return false;
   unsigned long long tq = P.trace ? gtimer2() : 0;
   const int policy = o.iarg[0];
   const double cut = (policy == 2) ? o.farg[1] : 1e-14;
@@ -1044,7 +1099,7 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
     Gs = G;
     ldgs = lg;
   } else {
-    double* Mc = ws + 8 * l + 2 * l * l + 200000;  // copy of M (ld m)
+    double* Mc = ws + 8 * l + 2 * l * l + D2LR_EXTRA;  // copy of M (ld m)
     FOR_MN(i, j, m, n) Mc[i + (int64_t)j * m] = M[i + (int64_t)j * ldm];
     WsGqr a;
     a.tp = take(KC + 1); a.wd = take(KC + 1); a.rd = take(KC + 1);
@@ -1056,7 +1111,8 @@ __device__ __noinline__ bool d2lr_big(const DevPlan& P, const hmx_op& o, int m, 
     gsm = take(GEMM_SMEM_DOUBLES);
     __syncthreads();
     if (m <= 256) k = ws_gqr<8>(m, n, M, ldm, thr, KC + 1, a);
-    else k = ws_gqr<16>(m, n, M, ldm, thr, KC + 1, a);
+    else if (m <= 512) k = ws_gqr<16>(m, n, M, ldm, thr, KC + 1, a);
+    else k = ws_gqr<32>(m, n, M, ldm, thr, KC + 1, a);
     if (k > KC) {  // revealed rank beyond this path: restore M, the caller falls back
       FOR_MN(i, j, m, n) M[i + (int64_t)j * ldm] = Mc[i + (int64_t)j * m];
       __syncthreads();
@@ -1240,6 +1296,9 @@ __device__ __noinline__ bool d2lr_ws(const DevPlan& P, const hmx_op& o, int m, i
   if (r < 0) {
     // the revealed rank does not fit the shared-memory core: the factored
     // block (still in shared memory) continues on the fat core
+#if !HMX_D2LR_HANDOFF
+    return false;
+#endif
     if (w.cap2 < GEMM_SMEM_DOUBLES) return false;
     return d2lr_tail(P, o, m, n, k, w.G, w.lg, w.tpg, w.wdg, w.rdg, w.perm, w.pos, Uo, lduo, Vo, ldvo, rslot,
                      ws, sm, w.free2, tq);
@@ -1266,7 +1325,7 @@ __device__ void op_d2lr(const DevPlan& P, const Cx& c, const hmx_op& o, double* 
   double* ws = mref(P, c, o.wref);
 #if HMX_WS
   if (d2lr_ws(P, o, m, n, M, ldm, Uo, o.ld[2], Vo, o.ld[3], rslot, ws, sm)) return;
-#if HMX_WS > 1
+#if HMX_WS > 1 && HMX_D2LR_BIG
   if (d2lr_big(P, o, m, n, M, ldm, Uo, o.ld[2], Vo, o.ld[3], rslot, ws, sm)) return;
 #endif
 #endif
@@ -2415,7 +2474,7 @@ hmx_status hmx_dense_to_lowrank_batched(int32_t batch, int32_t m, int32_t n, con
   if (batch < 0 || m <= 0 || n <= 0 || cap < 0) return HMX_ERR_ARG;
   const int64_t s = std::min(m, n), l = std::max(m, n);
   const int64_t offW = (int64_t)m * n;
-  const int64_t scratch = offW + 8 * l + (l >= 256 ? 3 * l * l + 200000 : 16 * l * l);
+  const int64_t scratch = offW + 8 * l + (l >= 256 ? 3 * l * l + 2500000 : 16 * l * l);
   MiniRun mr;
   for (int b = 0; b < batch; ++b) {
     hmx_op c1 = blank(OP_COPY);

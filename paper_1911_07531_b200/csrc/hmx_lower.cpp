@@ -325,7 +325,7 @@ struct Lower {
   void d2lr(int64_t m, int64_t n, const Ref& M, const Ref& Uo, const Ref& Vo, int32_t rslot, int64_t cp) {
     const int64_t l = std::max(m, n);
     // blocks of 256 and more keep a copy of M next to the work area (d2lr_big)
-    Ref ws = sref(8 * l + (l >= 256 ? 3 * l * l + 200000 : 16 * l * l), 1);
+    Ref ws = sref(8 * l + (l >= 256 ? 3 * l * l + 2500000 : 16 * l * l), 1);
     hmx_op& o = op(OP_D2LR);
     o.dim[0] = (int32_t)m; o.dim[1] = (int32_t)n;
     o.ld[0] = M.ld; o.ld[2] = Uo.ld; o.ld[3] = Vo.ld;

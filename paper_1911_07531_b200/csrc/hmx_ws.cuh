@@ -623,7 +623,7 @@ __device__ void ws_jacobi_rounds(int rows, int k, double* X, int ldx, double tol
 }
 
 // Returns false if not converged after 60 sweeps.  sigma / order as in
-// cta_jacobi_svd.  rows <= 256.
+// cta_jacobi_svd.  rows <= 512.
 __device__ bool ws_jacobi(int rows, int k, double* X, int ldx, double* sigma, int* order, int* flag,
                           int* sweeps_out) {
   // A sweep whose pairs all arrive with cosines <= HMX_WS_JTOL is the last
@@ -645,7 +645,8 @@ __device__ bool ws_jacobi(int rows, int k, double* X, int ldx, double* sigma, in
     if (npairs * 32 <= HMX_THREADS || rows > 128) {
       if (rows <= 64) ws_jacobi_rounds<32, 2>(rows, k, X, ldx, tol2, flag);
       else if (rows <= 128) ws_jacobi_rounds<32, 4>(rows, k, X, ldx, tol2, flag);
-      else ws_jacobi_rounds<32, 8>(rows, k, X, ldx, tol2, flag);
+      else if (rows <= 256) ws_jacobi_rounds<32, 8>(rows, k, X, ldx, tol2, flag);
+      else ws_jacobi_rounds<32, 16>(rows, k, X, ldx, tol2, flag);
     } else if (npairs * 16 <= HMX_THREADS || rows > 64) {
       if (rows <= 64) ws_jacobi_rounds<16, 4>(rows, k, X, ldx, tol2, flag);
       else ws_jacobi_rounds<16, 8>(rows, k, X, ldx, tol2, flag);

@@ -343,15 +343,13 @@ class Planner:
 
     def trunc(self, m, n, K, kb, U, V, Uo, Vo, rslot, cap):
         kb = max(int(kb), 1)
-        ws = self.sref(9 * kb * kb + (int(m) + int(n) + 200) * kb + 2048, 1)
+        ws = self.sref(L.trunc_scratch(m, n, kb), 1)
         self._op(OP_TRUNC, 0, (m, n, K, 0), (U.ld, V.ld, Uo.ld, Vo.ld), (U, V, Uo, Vo),
                  slots=(rslot, 0, 0, 0), iargs=(self.mode, self.kfix, cap, kb),
                  fargs=(0.0, self.eps), wref=ws)
 
     def d2lr(self, m, n, M, Uo, Vo, rslot, cap):
-        l = max(m, n)
-        # blocks of 256 and more keep a copy of M next to the work area (d2lr_big)
-        ws = self.sref(8 * l + (3 * l * l + 200000 if l >= 256 else 16 * l * l), 1)
+        ws = self.sref(L.d2lr_scratch(m, n), 1)
         self._op(OP_D2LR, 0, (m, n, 0, 0), (M.ld, 0, Uo.ld, Vo.ld), (M, None, Uo, Vo),
                  slots=(rslot, 0, 0, 0), iargs=(self.mode, self.kfix, cap, 0),
                  fargs=(0.0, self.eps), wref=ws)

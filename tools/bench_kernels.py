@@ -51,7 +51,7 @@ def run(ops_per_task, bases, scratch, reps=5, nt=None, trace=False):
 
 def trunc_case(m, n, K, decay=0.3, eps=1e-6, batch=int(os.environ.get('HMX_BENCH_BATCH', '148')), trace=False):
     rng = np.random.default_rng(0)
-    kb = K
+    kb = max(K, int(os.environ.get('HMX_BENCH_KB', '0')))
     U = rng.normal(size=(batch, K, m)) * np.exp(-decay * np.arange(K))[None, :, None]
     V = rng.normal(size=(batch, K, n))
     dU = torch.from_numpy(U.reshape(batch, -1)).cuda()
@@ -102,7 +102,7 @@ def d2lr_case(m, n, decay=0.15, eps=1e-6, batch=int(os.environ.get('HMX_BENCH_BA
     out = torch.zeros(batch, (m + n) * min(m, n), dtype=torch.float64, device="cuda")
     rk = torch.zeros(batch, dtype=torch.int32, device="cuda")
     l = max(m, n)
-    scratch = m * n + 8 * l + (3 * l * l + 200000 if l >= 256 else 16 * l * l)
+    scratch = m * n + 8 * l + (3 * l * l + 2500000 if l >= 256 else 16 * l * l)
     tasks = []
     for b in range(batch):
         o = np.zeros(2, dtype=_lib.OP_DTYPE)

@@ -18,10 +18,11 @@ cfg = configs.config(name)
 mode = mode or cfg.mode
 geom, root, perm, broot = configs.structure(cfg)
 pol = H.TruncationPolicy.fixed_accuracy(cfg.eps)
-A0 = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=64)
+RC = 128 if name.startswith("c5") else 64
+A0 = H.assemble(broot, configs.kernel(cfg, perm), pol, rank_cap=RC)
 split = int(os.environ.get("HMX_SPLIT", "256"))
-plan = get_plan(A0.table, mode, pol, 64, split_min=split)
-A = A0.copy(); L = H.zeros(broot, pol, 64); U = H.zeros(broot, pol, 64)
+plan = get_plan(A0.table, mode, pol, RC, split_min=split)
+A = A0.copy(); L = H.zeros(broot, pol, RC); U = H.zeros(broot, pol, RC)
 plan.run(A.store, L.store, U.store, exe)
 A.store.copy_from(A0.store)
 plan.plan.enable_trace(True)
