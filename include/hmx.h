@@ -54,6 +54,15 @@ typedef struct hmx_op {
   int64_t wref;             /* workspace ref (TRUNC / D2LR)               */
 } hmx_op; /* 128 bytes */
 
+/* Workspace (doubles) behind wref that the device paths assume:
+ *   OP_TRUNC (m x n, stacked capacity kb = iarg[3]):
+ *       9 kb^2 + (m + n + 200) kb + 2048
+ *   OP_D2LR  (m x n, l = max(m, n)):
+ *       8 l + 16 l^2                 (l < 256)
+ *       8 l + 3 l^2 + 2500000        (l >= 256: reflector blocks, R1^T, the
+ *                                     core's scratch and a copy of the block)
+ * (hmx_lower.cpp and _lib.py: trunc_scratch / d2lr_scratch use these.) */
+
 /* Library identity / capability. */
 const char* hmx_version(void);
 int hmx_op_size(void);
