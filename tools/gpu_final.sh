@@ -12,7 +12,8 @@ for cfg in c2 c1 c4 c5_d3; do
 done
 timeout 1500 python bench.py --impl reference > $O/reference_c3.json 2> $O/reference_c3.err
 # DMMA A/B: GEMM op latency / throughput and one c2 factorization with either GEMM variant
-for v in "" _dmma; do
+# (build the arms first: python tools/build_variant.py _dfma -DHMX_DMMA=0; _dmma -DHMX_DMMA=1)
+for v in _dfma _dmma; do
   lib=$PWD/paper_1911_07531_b200/libhmx$v.so
   HMX_LIB=$lib timeout 600 python tools/ab_gemm.py > $O/ab_gemm$v.log 2>&1
   HMX_LIB=$lib timeout 900 python bench.py --config c2 --no-cpu-baseline --no-e2e > $O/ab_c2$v.json 2> $O/ab_c2$v.err
@@ -27,7 +28,7 @@ timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:
   --log-file $O/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_launch.log 2>&1
 timeout 2400 ncu --set full --clock-control none --import-source on -k regex:k_persistent -s 3 -c 1 -f \
   -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
-for v in "" _dmma; do
+for v in _dfma _dmma; do
   lib=$PWD/paper_1911_07531_b200/libhmx$v.so
   HMX_LIB=$lib timeout 1200 ncu --clock-control none -k regex:k_tasks -c 1 -f \
     --metrics sm__inst_executed_pipe_fp64.sum,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum,sm__inst_executed.sum \

@@ -62,23 +62,23 @@ ab = [f"# {tag}: FP64 tensor-core (DMMA, mma.sync m8n8k4) vs DFMA register tiles
       "(`csrc/hmx_device.cuh`).  `tools/ab_gemm.py`: batched products, one CTA per product, 4 per SM.\n",
       "| shape (m x n x k) | DFMA us per CTA-op | DFMA TFLOP/s | DMMA us per CTA-op | DMMA TFLOP/s |", "|---|---|---|---|---|"]
 rows = {}
-for v in ("", "_dmma"):
+for v in ("_dfma", "_dmma"):
     for line in text(os.path.join(src, f"ab_gemm{v}.log")).splitlines():
         if line.startswith("GEMM"):
             p = line.split()
             rows.setdefault(p[1], {})[v] = (p[4], p[8])
 for k, d in rows.items():
-    a, b = d.get("", ("-", "-")), d.get("_dmma", ("-", "-"))
+    a, b = d.get("_dfma", ("-", "-")), d.get("_dmma", ("-", "-"))
     ab.append(f"| {k} | {a[0]} | {a[1]} | {b[0]} | {b[1]} |")
 ab.append("")
-for v, name in (("", "DFMA"), ("_dmma", "DMMA")):
+for v, name in (("_dfma", "DFMA"), ("_dmma", "DMMA")):
     d = jline(os.path.join(src, f"ab_c2{v}.json"))
     if d:
         par = d.get("parity") or {}
         ab.append(f"c2, one factorization, {name} build: {d.get('factor_time_s', 0):.4f} s, parity ok = {par.get('ok')} "
                   f"(rank mismatches {par.get('rank_mismatches')}).")
 ab.append("\nncu counters of one launch of the 256^3 batch (`--metrics`, `k_tasks<1>`):\n")
-for v, name in (("", "DFMA"), ("_dmma", "DMMA")):
+for v, name in (("_dfma", "DFMA"), ("_dmma", "DMMA")):
     p = os.path.join(src, f"ncu_gemm{v}.csv")
     if not os.path.exists(p):
         continue
