@@ -295,6 +295,11 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
 #ifndef HMX_GWIDE
 #define HMX_GWIDE 0
 #endif
+// narrowest column block the fat truncation accepts (tall factors need many
+// narrow blocks, each re-applying all previous ones)
+#ifndef HMX_FAT_MINNB
+#define HMX_FAT_MINNB 32
+#endif
 #ifndef HMX_WS
 #define HMX_WS 3  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path, 3: + fat path
 #endif
@@ -935,7 +940,7 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
   const int nbu = ws_cb_nb(m, K, P.smem_work), nbv = ws_cb_nb(n, K, P.smem_work);
   // tall factors would need many narrow column blocks, each re-applying all
   // previous ones from global memory: they stay with the blocked path
-  if (nbu < min(32, (K + 7) & ~7) || nbv < min(32, (K + 7) & ~7)) return false;
+  if (nbu < min(HMX_FAT_MINNB, (K + 7) & ~7) || nbv < min(HMX_FAT_MINNB, (K + 7) & ~7)) return false;
   const int rcap = min(min(p, q), max(o.iarg[2], 1));
   if (fat_core_need(p, q, min(nbu, p), min(nbv, q), rcap) > P.smem_work) return false;
   // global workspace (planner: 9 kb^2 + (m + n + 200) kb + 2048 doubles):
