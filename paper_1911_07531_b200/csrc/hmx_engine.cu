@@ -300,6 +300,10 @@ __device__ void recompose_jobs(int r, int p, int q, int m, int n, int kg, const 
 #ifndef HMX_FAT_MINNB
 #define HMX_FAT_MINNB 32
 #endif
+// largest stacked rank the fat truncation takes (cores above 120 run from L2)
+#ifndef HMX_FAT_KMAX
+#define HMX_FAT_KMAX 128
+#endif
 #ifndef HMX_WS
 #define HMX_WS 3  // 0: step-synchronous paths only, 1: + shared-memory path, 2: + panel (TSQR) path, 3: + fat path
 #endif
@@ -936,7 +940,7 @@ __device__ __noinline__ bool trunc_ws_fat(const DevPlan& P, const hmx_op& o, int
                                           int ldvo, int* rslot, double* ws, int64_t kb, double* sm,
                                           unsigned long long& tq) {
   const int p = min(m, K), q = min(n, K);
-  if (K > 128 || p > 128 || q > 128 || K < 8) return false;
+  if (K > HMX_FAT_KMAX || p > HMX_FAT_KMAX || q > HMX_FAT_KMAX || K < 8) return false;
   const int nbu = ws_cb_nb(m, K, P.smem_work), nbv = ws_cb_nb(n, K, P.smem_work);
   // tall factors would need many narrow column blocks, each re-applying all
   // previous ones from global memory: they stay with the blocked path
