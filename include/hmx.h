@@ -61,7 +61,9 @@ typedef struct hmx_op {
  *       8 l + 16 l^2                 (l < 256)
  *       8 l + 3 l^2 + 2500000        (l >= 256: reflector blocks, R1^T, the
  *                                     core's scratch and a copy of the block)
- * (hmx_lower.cpp and _lib.py: trunc_scratch / d2lr_scratch use these.) */
+ * (hmx_lower.cpp and _lib.py: trunc_scratch / d2lr_scratch use these;
+ * hmx_op_workspace returns them, 0 for ops without workspace.) */
+int64_t hmx_op_workspace(int32_t code, int32_t m, int32_t n, int32_t kb);
 
 /* Library identity / capability. */
 const char* hmx_version(void);

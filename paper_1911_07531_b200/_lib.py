@@ -95,6 +95,7 @@ def lib():
     vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     sig = {
         "hmx_version": ([], C.c_char_p),
+        "hmx_op_workspace": ([i32, i32, i32, i32], i64),
         "hmx_op_size": ([], C.c_int),
         "hmx_getrf_nopiv_batched": ([i32, i32, vp, i32, i64, vp, vp, i64, vp, vp], i32),
         "hmx_trsm_lower_unit_batched": ([i32, i32, i32, vp, i32, i64, vp, i32, i64, vp], i32),
@@ -138,7 +139,7 @@ def lib():
 
 
 EXPORTED = (
-    "hmx_version", "hmx_op_size", "hmx_getrf_nopiv_batched", "hmx_trsm_lower_unit_batched",
+    "hmx_version", "hmx_op_size", "hmx_op_workspace", "hmx_getrf_nopiv_batched", "hmx_trsm_lower_unit_batched",
     "hmx_trsm_upper_trans_batched", "hmx_trsm_upper_batched", "hmx_gemm_batched", "hmx_truncate_batched",
     "hmx_dense_to_lowrank_batched", "hmx_svd_values_batched", "hmx_plan_create",
     "hmx_plan_bind", "hmx_plan_execute", "hmx_plan_status", "hmx_plan_counters",

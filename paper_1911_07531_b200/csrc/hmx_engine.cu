@@ -1948,6 +1948,19 @@ const char* hmx_version(void) {
 }
 int hmx_op_size(void) { return (int)sizeof(hmx_op); }
 
+int64_t hmx_op_workspace(int32_t code, int32_t m, int32_t n, int32_t kb) {
+  // what the device paths assume behind op.wref (doubles); planners size it with this
+  if (code == OP_TRUNC) {
+    const int64_t k = kb > 0 ? kb : 1;
+    return 9 * k * k + ((int64_t)m + n + 200) * k + 2048;
+  }
+  if (code == OP_D2LR) {
+    const int64_t l = m > n ? m : n;
+    return 8 * l + (l >= 256 ? 3 * l * l + D2LR_EXTRA : 16 * l * l);
+  }
+  return 0;
+}
+
 hmx_status hmx_plan_create(const hmx_plan_desc* d, hmx_plan_t* out) {
   if (!d || !out || d->n_tasks < 0) return HMX_ERR_ARG;
   cudaError_t e = set_attrs();

@@ -55,3 +55,18 @@ def test_dag_library_exports_its_header():
     dl = ctypes.CDLL(_build.build_dag())
     missing = [n for n in names if not hasattr(dl, n)]
     assert not missing, missing
+
+
+def test_op_workspace_formulas_agree():
+    """The planners (Python: _lib.trunc_scratch / d2lr_scratch; native:
+    hmx_lower.cpp, checked op for op against the Python planner in
+    test_lower_cpu) size the TRUNC / D2LR workspaces with the formulas the
+    device paths assume (hmx_op_workspace): a smaller workspace is overrun."""
+    from paper_1911_07531_b200 import _lib
+
+    L = _lib.lib()
+    for m, n in ((64, 64), (128, 96), (128, 128), (200, 255), (256, 256), (512, 300), (1024, 1024), (4096, 2048)):
+        assert L.hmx_op_workspace(_lib.OP_D2LR, m, n, 0) == _lib.d2lr_scratch(m, n)
+        for kb in (1, 16, 64, 200):
+            assert L.hmx_op_workspace(_lib.OP_TRUNC, m, n, kb) == _lib.trunc_scratch(m, n, kb)
+    assert L.hmx_op_workspace(_lib.OP_GEMM, 64, 64, 0) == 0
