@@ -1371,6 +1371,36 @@ __device__ void op_svals(const DevPlan& P, const Cx& c, const hmx_op& o, double*
   svd_lowrank(P, o, p, q, W, p, ws, sm + 32, P.smem_work, nullptr, 0, nullptr, 0, sm, out);
 }
 
+#ifndef HMX_CBATCH2
+#define HMX_CBATCH2 1
+#endif
+// D (M x k) = alpha * S shifted down by r0 rows (rows outside [r0, r0 + mq) zero),
+// optionally added to D: four independent loads in flight per lane (the
+// plain loops wait ~700 cycles of L2 latency per element).  Own function: its
+// registers do not count against the interpreter's.
+__device__ __noinline__ void cta_copy_pad(int M, int k, double alpha, const double* S, int64_t lds, int r0, int mq,
+                                          double* D, int64_t ldd, bool add) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = w; t < k; t += HMX_WARPS) {
+    const double* s_ = S + (int64_t)t * lds - r0;
+    double* d_ = D + (int64_t)t * ldd;
+    for (int i = lane; i < M; i += 128) {
+      double v[4], c_[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ii = i + 32 * u;
+        v[u] = (ii < M && ii >= r0 && ii < r0 + mq) ? s_[ii] : 0.0;
+        c_[u] = (add && ii < M) ? d_[ii] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ii = i + 32 * u;
+        if (ii < M) d_[ii] = add ? fma(alpha, v[u], c_[u]) : alpha * v[u];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // one op
 // ---------------------------------------------------------------------------
@@ -1406,6 +1436,11 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
     }
     case OP_COPY: {
       const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]);
+#if HMX_CBATCH2
+      if (!(o.flags & F_TA))
+        cta_copy_pad(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], 0, m, mref(P, c, o.ref[2]), o.ld[2], false);
+      else
+#endif
       cta_copy(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], o.flags & F_TA,
                mref(P, c, o.ref[2]), o.ld[2]);
       __syncthreads();
@@ -1419,7 +1454,11 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
     }
     case OP_ADD: {
       const int m = dimv(P, c, o.dim[0]), n = dimv(P, c, o.dim[1]);
+#if HMX_CBATCH2
+      cta_copy_pad(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], 0, m, mref(P, c, o.ref[2]), o.ld[2], true);
+#else
       cta_add(m, n, o.farg[0], mref(P, c, o.ref[0]), o.ld[0], mref(P, c, o.ref[2]), o.ld[2]);
+#endif
       __syncthreads();
       break;
     }
@@ -1517,12 +1556,17 @@ __device__ void run_op(const DevPlan& P, const Cx& c, const hmx_op& o, double* s
       const double* Vs = mref(P, c, o.ref[1]);
       double* Ud = mref(P, c, o.ref[2]) + (int64_t)col0 * o.ld[2];
       double* Vd = mref(P, c, o.ref[3]) + (int64_t)col0 * o.ld[3];
+#if HMX_CBATCH2
+      cta_copy_pad(M, k, 1.0, Us, o.ld[0], r0, mq, Ud, o.ld[2], false);
+      cta_copy_pad(N, k, 1.0, Vs, o.ld[1], c0, nq, Vd, o.ld[3], false);
+#else
       FOR_MN(i, t, M, k)
         Ud[i + (int64_t)t * o.ld[2]] =
             (i >= r0 && i < r0 + mq) ? Us[(i - r0) + (int64_t)t * o.ld[0]] : 0.0;
       FOR_MN(i, t, N, k)
         Vd[i + (int64_t)t * o.ld[3]] =
             (i >= c0 && i < c0 + nq) ? Vs[(i - c0) + (int64_t)t * o.ld[1]] : 0.0;
+#endif
       __syncthreads();
       if (threadIdx.x == 0) *cnt = col0 + k;
       __syncthreads();
